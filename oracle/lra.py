@@ -1,0 +1,341 @@
+"""fp64 oracle of the hot path: Alg 10.2 (algrhtcur) with C-A iterations at stage 3
+(Remark rerfnhmt), maxvol by Alg D.2 stage 1 + Alg D.1, canonical nucleus (Alg 3.1),
+and the a-posteriori check ρ = ‖W − CUR‖_F / ‖W‖_F.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).  Plain numpy, fp64 / complex128, no
+blocking or fusion beyond what each cited definition states.  W is an (m, n) array whose
+values are converted exactly to fp64.  Index sets are int64 arrays in *slot order*.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .transforms import fourier_column_support, hadamard_column_support
+
+TAU = 1e-12   # tie slack of the pivot rule (reading C11 / R6)
+TOL = 1e-12   # dominance tolerance |c_ij| <= 1 + TOL (reading C12; BASELINE.json)
+
+
+class Singular(Exception):
+    """Exactly-zero / non-finite pivot, or σ_r(W[I,J]) = 0 (SPEC's 'singular generator')."""
+
+
+# ================================================================ stage 1: sketch
+def sketch(W: np.ndarray, mult: dict) -> np.ndarray:
+    """Y = W·M (Alg 10.2 stage 1; M = the realized multiplier).
+
+    ARHT: M = (D·H_{n,d}·P)[:, σ]; column c of Y is
+          Σ_{t<2^d} D_k·H[k,σ_c]·W[:,k] over the 2^d nonzeros k of column σ_c,
+          summed in ascending t (= ascending k).
+    ARFT: the same with Ω_{n,d} (complex128 result).
+    sparse: Σ_{t<nnz} sgn_{t,c}·W[:, row_{t,c}] in draw order (reading C7).
+    gaussian: Σ_{k<n} W[:,k]·Ω[k,:], accumulated sequentially in k.
+    The SRHT scale √(n/l̄) is omitted (reading C8: pivoting is scale-invariant)."""
+    W = np.asarray(W, dtype=np.float64)
+    m, n = W.shape
+    kind, lbar = mult["kind"], mult["lbar"]
+    if kind == "arht":
+        Y = np.zeros((m, lbar))
+        for c, sig in enumerate(mult["col"]):
+            rows, vals = hadamard_column_support(n, mult["depth"], int(sig))
+            for k, h in zip(rows, vals):
+                coef = float(mult["dsign"][k]) * h            # ±1
+                Y[:, c] = Y[:, c] + coef * W[:, k]
+        return Y
+    if kind == "arft":
+        Yr = np.zeros((m, lbar))
+        Yi = np.zeros((m, lbar))
+        for c, sig in enumerate(mult["col"]):
+            rows, vals = fourier_column_support(n, mult["depth"], int(sig))
+            for k, w in zip(rows, vals):
+                dk = float(mult["dsign"][k])
+                Yr[:, c] = Yr[:, c] + W[:, k] * (dk * w.real)
+                Yi[:, c] = Yi[:, c] + W[:, k] * (dk * w.imag)
+        return Yr + 1j * Yi
+    if kind == "sparse":
+        nnz = mult["nnz"]
+        Y = np.zeros((m, lbar))
+        for c in range(lbar):
+            for t in range(nnz):
+                k = int(mult["sp_row"][c * nnz + t])
+                Y[:, c] = Y[:, c] + float(mult["sp_sign"][c * nnz + t]) * W[:, k]
+        return Y
+    if kind == "gaussian":
+        Om = np.asarray(mult["omega"], dtype=np.float64)
+        Y = np.zeros((m, lbar))
+        for k in range(n):
+            Y = Y + np.outer(W[:, k], Om[k, :])
+        return Y
+    raise ValueError(kind)
+
+
+# ====================================================== maxvol (Alg D.2 + Alg D.1)
+@dataclass
+class MaxvolResult:
+    S: np.ndarray                 # slot-ordered selected rows
+    cert: float                   # max |C| at exit (dominance certificate)
+    swaps: int
+    lu_steps: int
+    cap_hit: bool
+    logdet: list = field(default_factory=list)   # log|det B[S,:]| after start and each swap
+
+
+def lup_pivots(B: np.ndarray, tau: float = TAU) -> np.ndarray:
+    """Cold start = Alg D.2 stage 1 on the tall block B (N×q): LU with
+    partial (row) pivoting.  Step t: M_t = max over unchosen rows of |B'[i,t]|;
+    p = smallest unchosen i with |B'[i,t]| ≥ (1−τ)·M_t (reading C11); then for every
+    unchosen i: B'[i,t:] −= (B'[i,t]/B'[p,t])·B'[p,t:]  (one IEEE multiply, one subtract)."""
+    Bp = np.array(B, dtype=np.complex128 if np.iscomplexobj(B) else np.float64)
+    N, q = Bp.shape
+    chosen = np.zeros(N, dtype=bool)
+    S = np.empty(q, dtype=np.int64)
+    for t in range(q):
+        a = np.abs(Bp[:, t])
+        a[chosen] = -1.0
+        M = a.max()
+        if not np.isfinite(M) or M <= 0.0:
+            raise Singular(f"LUP: zero/non-finite pivot at step {t}")
+        p = int(np.flatnonzero(a >= (1.0 - tau) * M)[0])
+        S[t] = p
+        chosen[p] = True
+        rest = ~chosen
+        f = Bp[rest, t] / Bp[p, t]
+        Bp[rest, t:] = Bp[rest, t:] - f[:, None] * Bp[p, t:][None, :]
+    return S
+
+
+def maxvol(B: np.ndarray, start=None, tau: float = TAU, tol: float = TOL, cap=None) -> MaxvolResult:
+    """Dominant q×q submatrix of the tall N×q block B (Alg D.1, transposed
+    to rows): from the start slots S (LUP cold start if None),
+      1. C = B·B[S,:]⁻¹ (from scratch); m* = max|C|; stop if m* ≤ 1+tol or cap reached;
+      2. (i*, j*) = smallest row-major index i·q+j with |C[i,j]| ≥ (1−τ)m*; S[j*] ← i*.
+    Each swap multiplies |det B[S,:]| by |C[i*,j*]| > 1."""
+    B = np.asarray(B)
+    N, q = B.shape
+    cap = 20 * q if cap is None else cap
+    if start is None:
+        S = lup_pivots(B, tau)
+        lu_steps = q
+    else:
+        S = np.array(start, dtype=np.int64).copy()
+        lu_steps = 0
+    swaps = 0
+    logdet = []
+    while True:
+        BS = B[S, :]
+        sign, ld = np.linalg.slogdet(BS)
+        if sign == 0 or not np.isfinite(ld):
+            raise Singular("maxvol: singular B[S,:]")
+        logdet.append(float(ld))
+        C = np.linalg.solve(BS.T, B.T).T          # C = B · B[S,:]⁻¹
+        absC = np.abs(C)
+        # C[S,:] = I_q exactly (Alg D.2 stage 2: C = (I_r | C')); the test and the swap
+        # search run over the non-selected rows C' only (stage 3, "||A'_1||_C <= 1").
+        absC[S, :] = 0.0
+        mstar = float(absC.max())
+        if mstar <= 1.0 + tol or swaps >= cap:
+            return MaxvolResult(S, mstar, swaps, lu_steps, mstar > 1.0 + tol, logdet)
+        flat = int(np.flatnonzero(absC.ravel() >= (1.0 - tau) * mstar)[0])
+        i, j = divmod(flat, q)
+        S[j] = i
+        swaps += 1
+
+
+# ======================================================= operands ("W or an entry oracle")
+class DenseOperand:
+    """W given densely (m×n)."""
+
+    def __init__(self, W):
+        self.W = np.asarray(W, dtype=np.float64)
+        self.m, self.n = self.W.shape
+
+    def rows(self, I):
+        return self.W[np.asarray(I), :]
+
+    def cols(self, J):
+        return self.W[:, np.asarray(J)]
+
+    def block(self, I, J):
+        return self.W[np.ix_(np.asarray(I), np.asarray(J))]
+
+
+class FactoredOperand:
+    """Entry oracle W_ij = A_{i,:}·B_{:,j} + E_ij with E in CSR (config 4); W never formed."""
+
+    def __init__(self, A, B, row_ptr, col, val):
+        self.A = np.asarray(A, dtype=np.float64)
+        self.B = np.asarray(B, dtype=np.float64)
+        self.row_ptr, self.col, self.val = np.asarray(row_ptr), np.asarray(col), np.asarray(val, dtype=np.float64)
+        self.m, self.n = self.A.shape[0], self.B.shape[1]
+
+    def _e_rows(self, I):
+        out = np.zeros((len(I), self.n))
+        for a, i in enumerate(I):
+            lo, hi = self.row_ptr[i], self.row_ptr[i + 1]
+            out[a, self.col[lo:hi]] = self.val[lo:hi]
+        return out
+
+    def rows(self, I):
+        I = np.asarray(I)
+        return self.A[I, :] @ self.B + self._e_rows(I)
+
+    def cols(self, J):
+        J = np.asarray(J)
+        out = self.A @ self.B[:, J]
+        pos = {int(j): c for c, j in enumerate(J)}
+        for i in range(self.m):
+            for e in range(self.row_ptr[i], self.row_ptr[i + 1]):
+                c = pos.get(int(self.col[e]))
+                if c is not None:
+                    out[i, c] += self.val[e]
+        return out
+
+    def block(self, I, J):
+        return self.rows(I)[:, np.asarray(J)]
+
+
+# ============================================================ C-A loops (stage 3)
+@dataclass
+class CAResult:
+    I: np.ndarray
+    J: np.ndarray
+    loops_done: int
+    lu_steps: int
+    swaps: int
+    cap_hits: int
+    cert_rows: float
+    cert_cols: float
+    logdet_steps: list      # log|det W[I,J]| after every C-A step (start of each maxvol)
+    steps: list             # per-maxvol (side, swaps)
+
+
+def cross_approx(op, k: int, l: int, sweeps: int, Y=None, I0=None, J0=None,
+                 tau: float = TAU, tol: float = TOL, cap=None) -> CAResult:
+    """Alg 10.2 stages 2–3 with C-A iterations at stage 3 (Remark rerfnhmt):
+      I ← maxvol(Y) cold (stage 2), or I ← I₀ given (Tests 2);
+      loop 1..T:  J ← maxvol(W[I,:]ᵀ, start = J if loop > 1)        (horizontal step)
+                  I ← maxvol(W[:,J],  start = I)                      (vertical step)
+                  stop early if neither step swapped (fixed point, reading C13).
+    J0 (optional) warm-starts the first horizontal step (restart from a previous result).
+    Reading C9: v1 requires k = l (square generators)."""
+    if k != l:
+        raise ValueError("v1 requires k == l")
+    if Y is not None:
+        res = maxvol(Y, None, tau, tol, cap)
+        I = res.S
+        lu, sw, ch = res.lu_steps, res.swaps, int(res.cap_hit)
+        steps = [("sketch", res.swaps)]
+    else:
+        I = np.array(I0, dtype=np.int64)
+        lu = sw = ch = 0
+        steps = []
+    J = None if J0 is None else np.array(J0, dtype=np.int64)
+    logdet_steps = []
+    cert_r = cert_c = float("nan")
+    loops = 0
+    for loop in range(sweeps):
+        rh = maxvol(op.rows(I).T, J, tau, tol, cap)
+        rv = maxvol(op.cols(rh.S), I, tau, tol, cap)
+        loops += 1
+        lu += rh.lu_steps + rv.lu_steps
+        sw += rh.swaps + rv.swaps
+        ch += int(rh.cap_hit) + int(rv.cap_hit)
+        steps += [("h", rh.swaps), ("v", rv.swaps)]
+        logdet_steps += rh.logdet + rv.logdet
+        J, I = rh.S, rv.S
+        cert_c, cert_r = rh.cert, rv.cert
+        if loop > 0 and rh.swaps == 0 and rv.swaps == 0:
+            break
+    return CAResult(I, J, loops, lu, sw, ch, cert_r, cert_c, logdet_steps, steps)
+
+
+# ============================================================ canonical nucleus
+def canonical_nucleus(G: np.ndarray, r: int):
+    """Alg 3.1 (algcnnncl): U = W_{k,l,r}⁺ from the SVD G = S Σ Tᵀ truncated to
+    the r largest singular values: U = T_r Σ_r⁻¹ S_rᵀ (l×k).  Returns (U, S_r, σ_r, T_r)."""
+    G = np.asarray(G, dtype=np.float64)
+    if not 0 < r <= min(G.shape):
+        raise ValueError("need 0 < r <= min(k, l)")
+    S, sv, Th = np.linalg.svd(G)
+    if not sv[r - 1] > 0.0:
+        raise Singular("sigma_r(W[I,J]) = 0")
+    Sr, sr, Tr = S[:, :r], sv[:r], Th[:r, :].T
+    U = (Tr / sr[None, :]) @ Sr.T
+    return U, Sr, sr, Tr
+
+
+def rank_r_factors(C: np.ndarray, R: np.ndarray, Sr, sr, Tr):
+    """CUR = A·B with A = C·T_r·Σ_r⁻¹ (m×r) and B = S_rᵀ·R (r×n)."""
+    A = (np.asarray(C, dtype=np.float64) @ Tr) / sr[None, :]
+    Bf = Sr.T @ np.asarray(R, dtype=np.float64)
+    return A, Bf
+
+
+# ============================================================ a-posteriori checks
+def cur_residual(W: np.ndarray, A: np.ndarray, B: np.ndarray, row_block: int = 1024):
+    """num² = Σ_ij (W_ij − (A·B)_ij)², den² = Σ_ij W_ij² in fp64 (eq. eqcur0, P:1153-1155;
+    the "dense audit"), row-block partials summed in block order.  ρ = √(num²/den²)."""
+    W = np.asarray(W)
+    m = W.shape[0]
+    num2 = 0.0
+    den2 = 0.0
+    for i0 in range(0, m, row_block):
+        Wb = np.asarray(W[i0:i0 + row_block], dtype=np.float64)
+        D = Wb - A[i0:i0 + row_block] @ B
+        num2 += float(np.sum(D * D))
+        den2 += float(np.sum(Wb * Wb))
+    return num2, den2
+
+
+def sampled_residual(op, A, B, ii, jj):
+    """Sampled estimate num²_est = (mn/Q)·Σ_q d_q², d_q = W(i_q,j_q) − A[i_q,:]·B[:,j_q]
+    over Q i.i.d. uniform pairs (the mn/Q extrapolation is SPEC S:280-288)."""
+    Q = len(ii)
+    w = np.array([op.block([i], [j])[0, 0] for i, j in zip(ii, jj)]) if not isinstance(op, DenseOperand) \
+        else op.W[ii, jj]
+    d = w - np.einsum("qt,tq->q", A[ii, :], B[:, jj])
+    return op.m * op.n / Q * float(np.sum(d * d))
+
+
+def factored_den2(op: FactoredOperand) -> float:
+    """Exact ‖W‖_F² for W = A·B + E:  tr((AᵀA)(BBᵀ)) + 2·Σ_{(i,j)∈E} E_ij (A·B)_ij + Σ E_ij²."""
+    G1 = op.A.T @ op.A
+    G2 = op.B @ op.B.T
+    t = float(np.sum(G1 * G2))
+    cross = 0.0
+    for i in range(op.m):
+        lo, hi = op.row_ptr[i], op.row_ptr[i + 1]
+        if hi > lo:
+            cross += float(np.dot(op.val[lo:hi], op.A[i, :] @ op.B[:, op.col[lo:hi]]))
+    return t + 2.0 * cross + float(np.dot(op.val, op.val))
+
+
+# ============================================================ whole path
+@dataclass
+class CurResult:
+    I: np.ndarray
+    J: np.ndarray
+    U: np.ndarray
+    A: np.ndarray
+    B: np.ndarray
+    num2: float
+    den2: float
+    ca: CAResult
+    Y: object = None
+
+    @property
+    def rho(self):
+        return float(np.sqrt(self.num2 / self.den2))
+
+
+def cur_pipeline(W, mult, r: int, k: int, l: int, sweeps: int, I0=None, residual=True) -> CurResult:
+    """Alg 10.2 + Remark rerfnhmt + Alg 3.1 + the full a-posteriori check, on dense W."""
+    op = DenseOperand(W)
+    Y = sketch(W, mult) if mult is not None else None
+    ca = cross_approx(op, k, l, sweeps, Y=Y, I0=I0)
+    U, Sr, sr, Tr = canonical_nucleus(op.block(ca.I, ca.J), r)
+    A, B = rank_r_factors(op.cols(ca.J), op.rows(ca.I), Sr, sr, Tr)
+    num2, den2 = cur_residual(W, A, B) if residual else (float("nan"), float("nan"))
+    return CurResult(ca.I, ca.J, U, A, B, num2, den2, ca, Y)

@@ -1,0 +1,133 @@
+"""Pins of the oracle's maxvol (Alg D.2 stage 1 + Alg D.1) and C-A loops.
+
+Brute force over all q-row subsets, LAPACK's partial pivoting, the dominance and volume
+statements of the paper, and hand traces — not the oracle's own formulas."""
+import itertools
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import synth
+from oracle import lra
+
+
+def _absdet(B, S):
+    return abs(np.linalg.det(B[list(S), :]))
+
+
+def test_q1_is_argmax_with_smallest_index_tie():
+    """q = 1: the 1×1 volume is |entry| (SPEC lup_ca example); ties → smallest index."""
+    B = np.array([[0.5], [-3.0], [2.0], [3.0], [-1.0]])
+    r = lra.maxvol(B)
+    assert list(r.S) == [1] and r.swaps == 0
+
+
+def test_hand_trace_swap():
+    """SPEC dominant_submatrix example A = [[1, 2]] (transposed): start {0} → one swap
+    → {1}, certificate 1/2 (Alg D.1 by hand)."""
+    B = np.array([[1.0], [2.0]])
+    r = lra.maxvol(B, start=[0])
+    assert list(r.S) == [1] and r.swaps == 1 and r.cert == pytest.approx(0.5)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lup_pivots_match_lapack_getrf(seed):
+    """Cold start = LU with partial pivoting; LAPACK dgetrf (max |pivot|, first on ties)
+    selects the same rows when there are no near-ties."""
+    g = np.random.default_rng(seed)
+    B = g.standard_normal((40, 7))
+    S = lra.lup_pivots(B)
+    lu, piv = scipy.linalg.lu_factor(B)
+    perm = np.arange(40)
+    for i, p in enumerate(piv):
+        perm[[i, p]] = perm[[p, i]]
+    assert list(S) == list(perm[:7])
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("N,q", [(8, 2), (10, 3), (12, 3)])
+def test_maxvol_vs_brute_force(seed, N, q):
+    """Exit state is dominant (|C'| ≤ 1+tol, Alg D.1 stage 1), locally maximal (no single
+    row swap raises |det| by more than 1+tol, Def. defmxv), and globally within q^{q/2}
+    of the maximum volume (Thm thlclglb with h = 1)."""
+    g = np.random.default_rng(1000 + seed)
+    B = g.standard_normal((N, q))
+    r = lra.maxvol(B)
+    C = B @ np.linalg.inv(B[r.S, :])
+    mask = np.ones(N, bool)
+    mask[r.S] = False
+    assert np.abs(C[mask]).max() <= 1 + 1e-12
+    v = _absdet(B, r.S)
+    vmax = max(_absdet(B, S) for S in itertools.combinations(range(N), q))
+    assert v >= vmax / q ** (q / 2) * (1 - 1e-12)
+    for j in range(q):
+        for i in range(N):
+            if i in r.S:
+                continue
+            S2 = list(r.S)
+            S2[j] = i
+            assert _absdet(B, S2) <= v * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_each_swap_multiplies_volume_by_c(seed):
+    """Each swap multiplies |det B[S,:]| by |c_{i*j*}| > 1: log-volume
+    strictly increases."""
+    g = np.random.default_rng(seed)
+    B = g.standard_normal((200, 10))
+    r = lra.maxvol(B, start=list(range(10)))
+    assert r.swaps > 0
+    assert all(b > a for a, b in zip(r.logdet, r.logdet[1:]))
+
+
+def test_dominant_start_is_fixed_point():
+    """A = (I_r | small) → the identity block is kept with 0 swaps (SPEC example)."""
+    g = np.random.default_rng(0)
+    B = np.vstack([np.eye(4), 0.1 * g.standard_normal((30, 4))])
+    r = lra.maxvol(B)
+    assert sorted(r.S) == [0, 1, 2, 3] and r.swaps == 0
+
+
+def test_singular_block_raises():
+    B = np.zeros((10, 3))
+    B[:, 0] = 1.0
+    with pytest.raises(lra.Singular):
+        lra.maxvol(B)
+
+
+def test_swap_cap_reported_not_error():
+    g = np.random.default_rng(3)
+    B = g.standard_normal((300, 8))
+    r = lra.maxvol(B, start=list(range(8)), cap=1)
+    assert r.swaps == 1 and r.cap_hit
+
+
+# ------------------------------------------------------------------ C-A loops
+def test_ca_two_step_volume_bound_brute_force():
+    """Thm th111 with thlclglb: after a C-A loop whose steps end dominant,
+    W[I,J] is (r^{r/2})²-maximal over ALL k×l submatrices (5×5, r = 2, brute force)."""
+    for seed in range(10):
+        W = np.random.default_rng(50 + seed).standard_normal((5, 5))
+        op = lra.DenseOperand(W)
+        ca = lra.cross_approx(op, 2, 2, 3, I0=[0, 1])
+        v = abs(np.linalg.det(op.block(ca.I, ca.J)))
+        vmax = max(abs(np.linalg.det(W[np.ix_(I, J)]))
+                   for I in itertools.combinations(range(5), 2) for J in itertools.combinations(range(5), 2))
+        assert v >= vmax / (2.0 ** 1) ** 2 * (1 - 1e-12)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_ca_log_volume_monotone_and_fixed_point(seed):
+    """Reading C10: warm starts make log|det W[I,J]| non-decreasing across C-A steps, and
+    a converged loop is a fixed point (0 swaps on the next loop)."""
+    W = synth.factor_gaussian(seed, 300, 200, 6, 1e-6)
+    op = lra.DenseOperand(W)
+    I0 = synth.random_rows(seed, 300, 6)
+    ca = lra.cross_approx(op, 6, 6, 6, I0=I0)
+    ld = ca.logdet_steps
+    assert all(b >= a - 1e-9 for a, b in zip(ld, ld[1:]))
+    assert ca.steps[-1][1] == 0 and ca.steps[-2][1] == 0
+    ca2 = lra.cross_approx(op, 6, 6, 2, I0=ca.I, J0=ca.J)
+    assert list(ca2.I) == list(ca.I) and list(ca2.J) == list(ca.J)
+    assert all(sw == 0 for _, sw in ca2.steps)

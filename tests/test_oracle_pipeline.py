@@ -1,0 +1,158 @@
+"""Pins of the oracle's nucleus, residual and whole path (configs 1–3 recipes)."""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import lra
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ nucleus (Alg 3.1)
+def test_nucleus_spec_examples():
+    """SPEC canonical_nucleus examples: [[5]] → 0.2; ones(2,2), r=1 → ones/4;
+    diag(3, 1e-9), r = 1 → diag(1/3, 0)."""
+    U, *_ = lra.canonical_nucleus(np.array([[5.0]]), 1)
+    assert U[0, 0] == pytest.approx(0.2, rel=1e-15)
+    U, *_ = lra.canonical_nucleus(np.ones((2, 2)), 1)
+    assert np.allclose(U, np.ones((2, 2)) / 4, atol=1e-15)
+    U, *_ = lra.canonical_nucleus(np.diag([3.0, 1e-9]), 1)
+    assert np.allclose(U, np.diag([1 / 3, 0.0]), atol=1e-15)
+
+
+def test_nucleus_is_inverse_when_k_eq_l_eq_r():
+    """Remark reklr_kl: k = l = r ⇒ U = W_{r,r}⁻¹ (eq. eqnucinv)."""
+    G = np.random.default_rng(1).standard_normal((6, 6))
+    U, *_ = lra.canonical_nucleus(G, 6)
+    assert np.allclose(U, np.linalg.inv(G), rtol=1e-12, atol=1e-12)
+
+
+def test_nucleus_penrose_identities():
+    """U = W_{k,l,r}⁺ satisfies the four Penrose identities with the truncation G_r."""
+    g = np.random.default_rng(2)
+    G = g.standard_normal((7, 5)) @ np.diag([5, 3, 1, 1e-3, 1e-4]) @ g.standard_normal((5, 7))
+    U, Sr, sr, Tr = lra.canonical_nucleus(G, 3)
+    s, sv, th = np.linalg.svd(G)
+    Gr = (s[:, :3] * sv[:3]) @ th[:3]
+    assert np.allclose(Gr @ U @ Gr, Gr, atol=1e-12)
+    assert np.allclose(U @ Gr @ U, U, atol=1e-10)
+    assert np.allclose((Gr @ U).T, Gr @ U, atol=1e-12)
+    assert np.allclose((U @ Gr).T, U @ Gr, atol=1e-12)
+
+
+# ------------------------------------------------------------------ residual
+def test_residual_brute_force_loops():
+    """num², den² against pure-Python triple loops on a tiny instance."""
+    g = np.random.default_rng(4)
+    W = g.standard_normal((7, 9)).astype(np.float32)
+    A = g.standard_normal((7, 3))
+    B = g.standard_normal((3, 9))
+    num2 = den2 = 0.0
+    for i in range(7):
+        for j in range(9):
+            s = 0.0
+            for t in range(3):
+                s += A[i, t] * B[t, j]
+            num2 += (float(W[i, j]) - s) ** 2
+            den2 += float(W[i, j]) ** 2
+    n2, d2 = lra.cur_residual(W, A, B, row_block=3)
+    assert n2 == pytest.approx(num2, rel=1e-13) and d2 == pytest.approx(den2, rel=1e-14)
+
+
+# ------------------------------------------------------------------ whole path
+@pytest.mark.parametrize("seed", range(10))
+def test_exact_recovery_rank_r(seed):
+    """Thm thcandec: rank-r W with a nonsingular generator ⇒ W = CUR."""
+    W = synth.factor_gaussian(seed, 120, 96, 5, 0.0)
+    M = synth.multiplier_abridged(seed, 96, 3, 5, "arht")
+    res = lra.cur_pipeline(W, M, 5, 5, 5, 2)
+    assert res.rho <= 1e-12
+
+
+def test_recovery_canonical_truncation_k_gt_r():
+    """k = l = 6 > r = 4 on rank-4 + 1e-12 noise: the canonical truncation (Alg 3.1)
+    recovers W to the noise level (Cor. cowc1), above the Eckart–Young floor."""
+    W = synth.factor_gaussian(3, 150, 128, 4, 1e-24)
+    M = synth.multiplier_abridged(3, 128, 2, 6, "arht")
+    res = lra.cur_pipeline(W, M, 4, 6, 6, 2)
+    sv = np.linalg.svd(W, compute_uv=False)
+    floor = np.sqrt(np.sum(sv[4:] ** 2) / np.sum(sv ** 2))
+    assert floor * (1 - 1e-6) <= res.rho <= 1e3 * floor
+
+
+def test_config1_baseline_expectations():
+    """BASELINE.json config 1: ρ ≤ 1e-9 and maxvol dominance ≤ 1 + 1e-12."""
+    W = synth.config1(0)
+    M = synth.multiplier_abridged(0, 256, 3, 8, "arht")
+    res = lra.cur_pipeline(W, M, 8, 8, 8, 2)
+    assert res.rho <= 1e-9
+    assert res.ca.cert_rows <= 1 + 1e-12 and res.ca.cert_cols <= 1 + 1e-12
+    # Eckart–Young floor (eq. eqnsgmrfr): ρ ≥ sqrt(Σ_{i>r} σ_i²)/‖W‖_F
+    sv = np.linalg.svd(W, compute_uv=False)
+    assert res.rho >= np.sqrt(np.sum(sv[8:] ** 2) / np.sum(sv ** 2)) * (1 - 1e-9)
+
+
+@pytest.mark.parametrize("kind", ["arht", "arft", "gaussian"])
+def test_config2_small_floor_and_dominance(kind):
+    """Config-2 recipe at n = 512: ρ above the Eckart–Young floor and within a modest
+    factor of it; every maxvol ends dominant."""
+    n = 512
+    W = synth.config2(0, n=n, p=160)
+    M = (synth.multiplier_gaussian(0, n, 48) if kind == "gaussian"
+         else synth.multiplier_abridged(0, n, 4, 48, kind))
+    res = lra.cur_pipeline(W, M, 32, 48, 48, 3)
+    sv = np.linalg.svd(np.asarray(W, np.float64), compute_uv=False)
+    floor = np.sqrt(np.sum(sv[32:] ** 2) / np.sum(sv ** 2))
+    assert floor * (1 - 1e-9) <= res.rho <= 20 * floor
+    assert res.ca.cert_rows <= 1 + 1e-12 and res.ca.cert_cols <= 1 + 1e-12
+
+
+def test_config3_block_floor():
+    s, t = synth.cauchy_params(0, 2)
+    for b in range(2):
+        W = synth.cauchy_block(s[b], t[b])
+        M = synth.multiplier_sparse_batch(0, 2, 512, 20)
+        Mb = dict(M, sp_row=M["sp_row"][b], sp_sign=M["sp_sign"][b])
+        res = lra.cur_pipeline(W, Mb, 16, 20, 20, 2)
+        sv = np.linalg.svd(np.asarray(W, np.float64), compute_uv=False)
+        floor = np.sqrt(np.sum(sv[16:] ** 2) / np.sum(sv ** 2))
+        assert floor * (1 - 1e-6) <= res.rho <= 1e-6
+
+
+def test_delta_matrices_defeat_superfast_ca():
+    """Example exdlt: a ±δ matrix whose nonzero lies outside the rows and
+    columns the algorithm reads gives a singular generator — reported, not hidden."""
+    pats = np.loadtxt(os.path.join(GOLD, "delta_matrices_2x2.txt"), comments="#")
+    assert pats.shape == (8, 4) and np.all(np.abs(pats).sum(axis=1) == 1)
+    W = np.zeros((8, 8))
+    W[6, 5] = 1.0
+    with pytest.raises(lra.Singular):
+        lra.cross_approx(lra.DenseOperand(W), 1, 1, 2, I0=[0])
+
+
+def test_sampled_residual_unbiased():
+    """num²_est = (mn/Q)Σd² over uniform samples tracks the full num²."""
+    W = synth.factor_gaussian(1, 300, 200, 4, 1e-4)
+    M = synth.multiplier_abridged(1, 200, 3, 4, "arht")
+    res = lra.cur_pipeline(W, M, 4, 4, 4, 2)
+    ii, jj = synth.sample_pairs(9, 300, 200, 200000)
+    est = lra.sampled_residual(lra.DenseOperand(W), res.A, res.B, ii, jj)
+    assert est == pytest.approx(res.num2, rel=0.02)
+
+
+def test_factored_operand_matches_dense():
+    """Config-4 entry oracle on a downsized instance equals the dense materialization;
+    the factored ‖W‖_F² identity equals the dense one."""
+    c4 = synth.config4(0, m=384, n=320, p=5, dens_ab=0.3, dens_e=0.01)
+    op = lra.FactoredOperand(c4["A"], c4["B"], c4["row_ptr"], c4["col"], c4["val"])
+    Wd = c4["A"] @ c4["B"]
+    for i in range(op.m):
+        lo, hi = c4["row_ptr"][i], c4["row_ptr"][i + 1]
+        Wd[i, c4["col"][lo:hi]] += c4["val"][lo:hi]
+    I = np.array([3, 100, 7])
+    J = np.array([0, 319, 31, 5])
+    assert np.allclose(op.rows(I), Wd[I], atol=1e-14)
+    assert np.allclose(op.cols(J), Wd[:, J], atol=1e-14)
+    assert lra.factored_den2(op) == pytest.approx(float(np.sum(Wd * Wd)), rel=1e-12)
