@@ -1,0 +1,180 @@
+/*
+ * lra.h — C-ABI of the B200-native superfast CUR hot path (arXiv 1710.07946).
+ *
+ * Citation keys: P:n = line n of the paper's LaTeX, with \label names.
+ * The path is Alg 10.2 ("algrhtcur") with C-A iterations at stage 3
+ * (Remark "rerfnhmt"), maxvol by Alg D.2 stage 1 + Alg D.1 ("alggos",
+ * "algdomin"), the canonical nucleus (Alg 3.1 "algcnnncl")
+ * and the a-posteriori check rho = ||W - CUR||_F / ||W||_F (eq. "eqcur0").
+ * DESIGN.md §2 lists every reading of the paper these functions implement.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless marked (host).  Matrices are COLUMN-MAJOR with
+ *    0-based int64 indices; index sets are int64 arrays in slot order.
+ *  - Ownership: every buffer is caller-owned; the library never frees caller memory.
+ *    Scratch belongs to the handle, grows on first use at a size, and is reused (no
+ *    allocation on the hot path once warm).
+ *  - Asynchrony: every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and returns after enqueueing.  Argument errors are returned
+ *    synchronously; numerical failures of the data-dependent loops (LRA_ESINGULAR, cap
+ *    hits) are written to device memory (lra_ca_stats.status, per-block status).
+ *  - On a non-OK status the outputs are unspecified.  lra_last_error() returns a
+ *    thread-local message describing the last non-OK status.
+ *  - There is no CPU fallback: without a CUDA device every call returns LRA_ECUDA.
+ */
+#ifndef LRA_H
+#define LRA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LRA_OK = 0,
+  LRA_EINVAL = -1,       /* shape / pointer / parameter violation                      */
+  LRA_ESINGULAR = -2,    /* zero or non-finite pivot, singular generator, sigma_r = 0  */
+  LRA_ENOMEM = -3,       /* scratch allocation failed                                  */
+  LRA_ECUDA = -4,        /* CUDA runtime error (incl. no device)                       */
+  LRA_ENCCL = -5,        /* reserved for the multi-GPU exchange                         */
+  LRA_EUNSUPPORTED = -6  /* valid input outside this build's tiers   */
+} lra_status;
+
+typedef enum { LRA_F32 = 0, LRA_F64 = 1 } lra_dtype;
+
+/* "W or an entry oracle" (the paper's input). */
+typedef enum { LRA_OP_DENSE = 0, LRA_OP_FACTORED_CSR = 1 } lra_op_kind;
+
+typedef struct {
+  int32_t kind;             /* lra_op_kind                                                    */
+  int32_t dtype;            /* lra_dtype of W's values (DENSE)                                */
+  int64_t m, n;             /* shape of W                                                     */
+  const void *w;            /* DENSE: m x n column-major, leading dimension ldw >= m          */
+  int64_t ldw;
+  /* FACTORED_CSR (config 4): W = A*B + E, never formed.  A m x p (ld m), B p x n (ld p),
+     fp64 values; E in CSR over rows: e_rowptr[m+1], e_col[nnz] (ascending per row), e_val. */
+  const double *fa, *fb;
+  int64_t p;
+  const int64_t *e_rowptr, *e_col;
+  const double *e_val;
+} lra_operand;
+
+/* Realized randomized multiplier M (n x lbar). */
+typedef enum {
+  LRA_MUL_NONE = 0,      /* no sketch: C-A starts from a given I0 (Tests 2)       */
+  LRA_MUL_GAUSSIAN = 1,  /* omega: n x lbar fp64 column-major (ld_omega)                       */
+  LRA_MUL_ARHT = 2,      /* (D H_{n,d} P)[:, col]: dsign[n] in {+1,-1}, col[lbar], 2^depth | n  */
+  LRA_MUL_ARFT = 3,      /* (D Omega_{n,d} P)[:, col]; Y is complex128                         */
+  LRA_MUL_SPARSE_PM1 = 4 /* column c: rows sp_row[c*nnz+t], signs sp_sign[c*nnz+t], t < nnz    */
+} lra_mul_kind;
+
+typedef struct {
+  int32_t kind;             /* lra_mul_kind                          */
+  int32_t depth;            /* d >= 1 (ARHT / ARFT)                  */
+  int64_t lbar;             /* number of sketch columns (== k == l)  */
+  const int8_t *dsign;      /* n entries                             */
+  const int64_t *col;       /* lbar sampled columns of T, in order   */
+  const int64_t *sp_row;    /* lbar * nnz_per_col                    */
+  const int8_t *sp_sign;    /* lbar * nnz_per_col                    */
+  int32_t nnz_per_col;
+  const double *omega;      /* GAUSSIAN                              */
+  int64_t ld_omega;
+} lra_multiplier;
+
+typedef struct lra_handle_s *lra_handle;
+
+/* Per-matrix statistics of lra_cross_approx / lra_batch (device memory). */
+typedef struct {
+  int32_t status;           /* LRA_OK or LRA_ESINGULAR                                       */
+  int32_t loops_done;       /* C-A loops executed (early exit on a fixed point, reading C13) */
+  int32_t lu_steps;         /* cold-start LUP steps (Alg D.2 stage 1)                        */
+  int32_t swaps;            /* Alg D.1 swaps over all maxvol calls                           */
+  int32_t cap_hits;         /* maxvol calls that stopped at the swap cap (not an error)      */
+  int32_t sketch_swaps;     /* swaps of the stage-2 maxvol on Y                              */
+  double cert_rows;         /* max |C'| at exit of the last vertical step   (<= 1 + tol)     */
+  double cert_cols;         /* max |C'| at exit of the last horizontal step (<= 1 + tol)     */
+} lra_ca_stats;
+
+typedef enum {
+  LRA_RECON_FAST = 0,    /* reserved: tensor-core reconstruction (not in this build)           */
+  LRA_RECON_PRECISE = 1  /* fp64-accurate reconstruction                                       */
+} lra_recon;
+
+/* Create a handle bound to CUDA device `device`.  nccl_unique_id must be NULL and
+   nranks == 1 in this build (multi-GPU runs deal independent problems to ranks, DESIGN.md
+   §9); other values return LRA_EUNSUPPORTED. */
+lra_status lra_handle_create(lra_handle *h /* host */, int device, const void *nccl_unique_id,
+                             int nranks, int rank);
+void lra_handle_destroy(lra_handle h);
+
+/* Stage 1 of Alg 10.2: Y = W * M, an m x lbar fp64 column-major matrix
+   (ARFT: complex128, interleaved re/im), leading dimension ldy >= m.  Sums run in a fixed
+   order (ascending t for ARHT/ARFT, draw order for SPARSE_PM1, ascending k for GAUSSIAN)
+   with fp64 accumulation; the SRHT scale sqrt(n/lbar) is omitted (reading C8).
+   Errors: EINVAL for null pointers, lbar < 1, 2^depth not dividing n, non-DENSE W. */
+lra_status lra_preprocess(lra_handle h, const lra_operand *W /* host struct */,
+                          const lra_multiplier *M /* host struct */, void *Y, int64_t ldy,
+                          void *stream);
+
+/* Stages 2-3 of Alg 10.2 with C-A at stage 3 (Remark rerfnhmt), then Alg 3.1:
+     I <- maxvol(Y) (cold)  or  I <- I0 (if Y == NULL);
+     for loop < sweeps:  J <- maxvol(W[I,:]^T, warm from J after loop 1)
+                         I <- maxvol(W[:,J],  warm from I);  stop when a later loop swaps nothing;
+     U = W_{k,l,r}^+ via the SVD W[I,J] = S Sigma T^T  (l x k, column-major),
+     A = W[:,J] T_r Sigma_r^{-1}  (m x r, ld m),   B = S_r^T W[I,:]  (r x n, ld r),
+   so that CUR = A*B.  maxvol: pivot rule = smallest row-major index among |c| >= (1-tie_slack)*max
+   (reading C11), stop when max |C'| <= 1 + swap_tol (C12), at most swap_cap swaps per call.
+   Requires 0 < r <= k == l (reading C9), k <= min(m, n), k <= 64.
+   y_complex != 0 means Y is complex128 (ARFT).  stats (device) may be NULL.
+   Errors: EINVAL / EUNSUPPORTED synchronously; ESINGULAR in stats->status. */
+lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy,
+                            int y_complex, const int64_t *I0, int64_t r, int64_t k, int64_t l,
+                            int32_t sweeps, double swap_tol, double tie_slack, int32_t swap_cap,
+                            int64_t *I, int64_t *J, double *U, double *A, double *B,
+                            lra_ca_stats *stats, void *stream);
+
+/* A-posteriori check (eq. eqcur0): num2 = sum_ij (W_ij - (A B)_ij)^2 and
+   den2 = sum_ij W_ij^2 in fp64 over the full matrix (nsamples == 0), or, when nsamples > 0,
+   num2 = (m n / Q) sum_q d_q^2 over the Q given pairs (si[q], sj[q]) and den2
+   = the exact ||W||_F^2 (dense: full pass; factored: tr((A^T A)(B B^T)) + 2 sum_E E.(AB) +
+   sum E^2).  num2, den2: device scalars.  prec must be LRA_RECON_PRECISE in this build. */
+lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A, const double *B,
+                            int64_t r, int32_t prec, int64_t nsamples, const int64_t *si,
+                            const int64_t *sj, double *num2, double *den2, void *stream);
+
+/* A batch of nb independent dense problems (config 3, FMM-style blocks): block b
+   is W0 with w = W0.w + b*w_stride elements (w_stride >= ldw*n).  SPARSE_PM1 multipliers may
+   differ per block: sp_row / sp_sign of block b start at b*m_stride entries; ARHT / ARFT /
+   GAUSSIAN blocks share one multiplier (m_stride must be 0).  Requires lbar == k.  Runs the
+   whole path (lra_preprocess, lra_cross_approx, lra_cur_residual) per block; outputs are
+   strided per block: I[b*k], J[b*l], U[b*l*k], num2[b], den2[b], stats[b] (may be NULL).
+   A block whose generator is singular gets stats[b].status = LRA_ESINGULAR and NaN num2/den2;
+   the other blocks are unaffected. */
+lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_stride,
+                     const lra_multiplier *M0, int64_t m_stride, int64_t r, int64_t k, int64_t l,
+                     int32_t sweeps, double swap_tol, double tie_slack, int32_t swap_cap,
+                     int32_t prec, int64_t *I, int64_t *J, double *U, double *num2, double *den2,
+                     lra_ca_stats *stats, void *stream);
+
+/* Kernel timing for measurement (bench.py): while enabled, every kernel this handle launches is
+   bracketed by a CUDA event pair recorded on its launch stream.  lra_profile_read synchronizes
+   on the recorded events, aggregates per kernel name (name -> total ms, launch count; at most
+   cap names, written to host arrays) and resets the record; returns the number of names or a
+   negative lra_status.  Enabling resets the record. */
+lra_status lra_profile_enable(lra_handle h, int enable);
+int lra_profile_read(lra_handle h, int cap, const char **names /* host */, double *ms /* host */,
+                     int64_t *counts /* host */);
+
+/* Thread-local message for the last non-OK status (never NULL). */
+const char *lra_last_error(void);
+
+/* Number of kernels this library has launched since the handle was created (host counter;
+   used by bench.py to report gpu_launches). */
+int64_t lra_launch_count(lra_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRA_H */

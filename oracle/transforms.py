@@ -99,7 +99,8 @@ def fourier_column_support(n: int, d: int, sigma: int):
     t = np.arange(q)
     rows = q * (sigma % s) + t
     e = (t * sigma) % n
-    return rows, np.exp(2j * np.pi * e / n)
+    ang = (2.0 * np.pi * e.astype(np.float64)) / float(n)   # fl(fl(2π·e)/n)
+    return rows, np.cos(ang) + 1j * np.sin(ang)
 
 
 def multiplier_dense(mult: dict, n: int) -> np.ndarray:

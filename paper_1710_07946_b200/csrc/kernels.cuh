@@ -1,0 +1,104 @@
+// kernels.cuh — argument blocks and launchers shared by the kernel files and lra_api.cu.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace lra {
+
+// Per-handle kernel timing (lra_profile_*): a CUDA event pair recorded on the launch
+// stream around every kernel while enabled; read back (and reset) by lra_profile_read.
+struct Prof {
+  int on = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char *> name;
+  size_t used = 0;
+  void begin(const char *nm, cudaStream_t st) {
+    if (!on) return;
+    grow();
+    name[used / 2] = nm;
+    cudaEventRecord(ev[used++], st);
+  }
+  void end(cudaStream_t st) {
+    if (!on) return;
+    cudaEventRecord(ev[used++], st);
+  }
+  void grow() {
+    if (used + 2 <= ev.size()) return;
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    name.resize(ev.size() / 2);
+  }
+};
+
+struct SketchArgs {
+  int kind, dtype, depth, nnz;
+  int64_t m, n, lbar, ldw, ldy;
+  const void *w;
+  int64_t w_stride;                 // batch stride of W (elements)
+  const int8_t *dsign;
+  const int64_t *col, *sp_row;
+  const int8_t *sp_sign;
+  int64_t m_stride;                 // batch stride of the multiplier arrays (entries)
+  void *y;
+  int64_t y_stride;                 // batch stride of Y (elements of double / double2)
+};
+cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st, Prof *pf);
+
+struct CAArgs {
+  OpView op;
+  int64_t w_stride;            // batch stride of dense W (elements)
+  const void *Y;               // sketch (m x q, column-major, fp64 / complex128) or null
+  int64_t ldy, y_stride;
+  int y_complex;
+  const int64_t *I0;           // used iff Y == null
+  int64_t i0_stride;
+  int q, sweeps, cap, cs, rpc, qp;
+  double tol, tau;
+  int64_t *I, *J;              // outputs, stride q per problem
+  lra_ca_stats *stats;         // per problem, may be null
+  int32_t *status;             // per problem
+};
+cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
+
+struct NucArgs {
+  OpView op;
+  int64_t w_stride;
+  const int64_t *I, *J;   // stride q per problem
+  int k, l, r;
+  double *U;              // l x k per problem (stride l*k), may be null
+  double *TS, *Sr;        // scratch: l x r and k x r per problem
+  int32_t *status;        // per problem: already LRA_ESINGULAR -> skip
+};
+struct FacArgs {
+  OpView op;
+  int64_t w_stride;
+  const int64_t *I, *J;
+  int k, l, r;
+  const double *TS, *Sr;
+  double *A, *B;            // A: m x r (lda = m) per problem; B: r x n (ld r) per problem
+  int64_t a_stride, b_stride;
+  const int32_t *status;
+};
+cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf);
+
+struct ResArgs {
+  int dtype;
+  int64_t m, n, ldw, w_stride;
+  const void *w;
+  const double *A, *B;       // per problem: A + b*a_stride (lda = m), B + b*b_stride (ld r)
+  int64_t a_stride, b_stride;
+  int r;
+  int64_t tiles_m, tiles_n;  // tiles per problem
+  double2 *partial;          // per problem per tile: (num2, den2)
+  const int32_t *status;
+};
+cudaError_t launch_residual(ResArgs a, int64_t nb, double *num2, double *den2, cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,
+                           const int64_t *sj, int64_t Q, double2 *partial, int nblk, double *num2,
+                           double *den2, cudaStream_t st, int *nlaunch, Prof *pf);
+
+}  // namespace lra

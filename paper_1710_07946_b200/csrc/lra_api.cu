@@ -1,0 +1,458 @@
+// lra_api.cu — the C-ABI of liblra.so (include/lra.h): handle, scratch, argument checks
+// and the launch sequence of each entry point.  No compute happens on the host.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cstdarg>
+
+#include "kernels.cuh"
+
+
+
+using namespace lra;
+
+static thread_local std::string g_err = "no error";
+
+static lra_status fail(lra_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(LRA_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));   \
+  } while (0)
+
+struct lra_handle_s {
+  int device;
+  int nranks, rank;
+  int64_t launches;
+  Prof prof;
+  // scratch arena (grows; reused)
+  void *ws;
+  size_t ws_bytes;
+};
+
+static lra_status ws_reserve(lra_handle h, size_t bytes) {
+  if (bytes <= h->ws_bytes) return LRA_OK;
+  if (h->ws) cudaFree(h->ws);
+  h->ws = nullptr;
+  h->ws_bytes = 0;
+  size_t want = bytes + bytes / 4;
+  if (cudaMalloc(&h->ws, want) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LRA_ENOMEM, "cannot allocate %zu bytes of scratch", want);
+  }
+  h->ws_bytes = want;
+  return LRA_OK;
+}
+
+struct Carve {
+  char *base;
+  size_t off;
+  template <typename T>
+  T *take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T *p = reinterpret_cast<T *>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+static OpView make_view(const lra_operand *W) {
+  OpView v{};
+  v.kind = W->kind;
+  v.dtype = W->dtype;
+  v.m = W->m;
+  v.n = W->n;
+  v.w = W->w;
+  v.ldw = W->ldw;
+  v.f.fa = W->fa;
+  v.f.fb = W->fb;
+  v.f.m = W->m;
+  v.f.p = W->p;
+  v.f.rowptr = W->e_rowptr;
+  v.f.col = W->e_col;
+  v.f.val = W->e_val;
+  return v;
+}
+
+static lra_status check_operand(const lra_operand *W) {
+  if (!W) return fail(LRA_EINVAL, "null operand");
+  if (W->m < 1 || W->n < 1) return fail(LRA_EINVAL, "empty operand (m=%lld, n=%lld)", (long long)W->m, (long long)W->n);
+  if (W->kind == LRA_OP_DENSE) {
+    if (!W->w) return fail(LRA_EINVAL, "dense operand with null w");
+    if (W->ldw < W->m) return fail(LRA_EINVAL, "ldw < m");
+    if (W->dtype != LRA_F32 && W->dtype != LRA_F64) return fail(LRA_EINVAL, "bad dtype");
+  } else if (W->kind == LRA_OP_FACTORED_CSR) {
+    if (!W->fa || !W->fb || !W->e_rowptr || W->p < 1) return fail(LRA_EINVAL, "factored operand incomplete");
+  } else {
+    return fail(LRA_EINVAL, "bad operand kind");
+  }
+  return LRA_OK;
+}
+
+static lra_status check_device(lra_handle h) {
+  if (!h) return fail(LRA_EINVAL, "null handle");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(LRA_ECUDA, "no CUDA device (this library has no CPU fallback)");
+  }
+  CK(cudaSetDevice(h->device));
+  return LRA_OK;
+}
+
+static lra_status check_mult(const lra_multiplier *M, int64_t n) {
+  if (!M) return fail(LRA_EINVAL, "null multiplier");
+  if (M->lbar < 1 || M->lbar > n) return fail(LRA_EINVAL, "lbar out of range");
+  switch (M->kind) {
+    case LRA_MUL_ARHT:
+    case LRA_MUL_ARFT:
+      if (M->depth < 1 || M->depth > 6 || (n % ((int64_t)1 << M->depth)) != 0)
+        return fail(LRA_EINVAL, "need 1 <= depth <= 6 and 2^depth | n (reading C21)");
+      if (!M->dsign || !M->col) return fail(LRA_EINVAL, "ARHT/ARFT needs dsign and col");
+      return LRA_OK;
+    case LRA_MUL_SPARSE_PM1:
+      if (!M->sp_row || !M->sp_sign || M->nnz_per_col < 1 || M->nnz_per_col > 64)
+        return fail(LRA_EINVAL, "sparse multiplier needs sp_row, sp_sign, 1 <= nnz <= 64");
+      return LRA_OK;
+    case LRA_MUL_GAUSSIAN:
+      if (!M->omega || M->ld_omega < n) return fail(LRA_EINVAL, "gaussian multiplier needs omega, ld >= n");
+      return LRA_OK;
+    default:
+      return fail(LRA_EINVAL, "bad multiplier kind");
+  }
+}
+
+static SketchArgs make_sketch(const lra_operand *W, const lra_multiplier *M, void *Y, int64_t ldy) {
+  SketchArgs a{};
+  a.kind = M->kind;
+  a.dtype = W->dtype;
+  a.depth = M->depth;
+  a.nnz = M->nnz_per_col;
+  a.m = W->m;
+  a.n = W->n;
+  a.lbar = M->lbar;
+  a.ldw = W->ldw;
+  a.ldy = ldy;
+  a.w = W->w;
+  a.dsign = M->dsign;
+  a.col = M->col;
+  a.sp_row = M->sp_row;
+  a.sp_sign = M->sp_sign;
+  a.y = Y;
+  return a;
+}
+
+extern "C" {
+
+const char *lra_last_error(void) { return g_err.c_str(); }
+
+lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_id, int nranks, int rank) {
+  if (!h) return fail(LRA_EINVAL, "null handle pointer");
+  *h = nullptr;
+  if (nccl_unique_id != nullptr || nranks != 1 || rank != 0)
+    return fail(LRA_EUNSUPPORTED, "in-library NCCL exchange is not in this build (nranks must be 1)");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(LRA_ECUDA, "no CUDA device (this library has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) return fail(LRA_EINVAL, "bad device %d", device);
+  CK(cudaSetDevice(device));
+  lra_handle_s *p = new lra_handle_s();
+  p->device = device;
+  p->nranks = nranks;
+  p->rank = rank;
+  *h = p;
+  return LRA_OK;
+}
+
+void lra_handle_destroy(lra_handle h) {
+  if (!h) return;
+  if (h->ws) cudaFree(h->ws);
+  for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
+  delete h;
+}
+
+lra_status lra_profile_enable(lra_handle h, int enable) {
+  if (!h) return fail(LRA_EINVAL, "null handle");
+  h->prof.on = enable ? 1 : 0;
+  h->prof.used = 0;
+  return LRA_OK;
+}
+
+int lra_profile_read(lra_handle h, int cap, const char **names, double *ms, int64_t *counts) {
+  if (!h) return fail(LRA_EINVAL, "null handle");
+  Prof &p = h->prof;
+  int nd = 0;
+  for (size_t i = 0; i + 1 < p.used; i += 2) {
+    float t = 0.f;
+    if (cudaEventSynchronize(p.ev[i + 1]) != cudaSuccess || cudaEventElapsedTime(&t, p.ev[i], p.ev[i + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LRA_ECUDA, "profile event read failed");
+    }
+    const char *nm = p.name[i / 2];
+    int d = 0;
+    while (d < nd && strcmp(names[d], nm) != 0) ++d;
+    if (d == nd) {
+      if (nd == cap) continue;
+      names[nd] = nm;
+      ms[nd] = 0.0;
+      counts[nd] = 0;
+      ++nd;
+    }
+    ms[d] += t;
+    counts[d] += 1;
+  }
+  p.used = 0;
+  return nd;
+}
+
+int64_t lra_launch_count(lra_handle h) { return h ? h->launches : 0; }
+
+lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multiplier *M, void *Y, int64_t ldy,
+                          void *stream) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  if ((s = check_operand(W)) != LRA_OK) return s;
+  if (W->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "lra_preprocess needs a dense operand");
+  if ((s = check_mult(M, W->n)) != LRA_OK) return s;
+  if (!Y || ldy < W->m) return fail(LRA_EINVAL, "Y null or ldy < m");
+  SketchArgs a = make_sketch(W, M, Y, ldy);
+  CK(launch_sketch(a, 1, M->omega, M->ld_omega, (cudaStream_t)stream, &h->prof));
+  h->launches += 1;
+  return LRA_OK;
+}
+
+static lra_status check_ca_shape(const lra_operand *W, int64_t r, int64_t k, int64_t l, int32_t sweeps) {
+  if (k != l) return fail(LRA_EINVAL, "v1 requires k == l (reading C9)");
+  if (r < 1 || r > k) return fail(LRA_EINVAL, "need 0 < r <= k");
+  if (k > W->m || l > W->n) return fail(LRA_EINVAL, "need k <= m and l <= n");
+  if (k > LRA_QMAX) return fail(LRA_EUNSUPPORTED, "k > %d is outside this build's maxvol tiers", LRA_QMAX);
+  if (sweeps < 1) return fail(LRA_EINVAL, "sweeps >= 1");
+  return LRA_OK;
+}
+
+// The whole C-A -> nucleus -> factors chain for nb problems sharing shapes.
+static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride, const void *Y, int64_t ldy,
+                            int64_t y_stride, int y_complex, const int64_t *I0, int64_t r, int64_t k,
+                            int32_t sweeps, double tol, double tau, int32_t cap, int64_t *I, int64_t *J,
+                            double *U, double *A, double *B, int64_t a_stride, int64_t b_stride,
+                            lra_ca_stats *stats, int32_t *status, double *TS, double *Sr, int64_t nb,
+                            cudaStream_t st) {
+  CAArgs ca{};
+  ca.op = make_view(W);
+  ca.w_stride = w_stride;
+  ca.Y = Y;
+  ca.ldy = ldy;
+  ca.y_stride = y_stride;
+  ca.y_complex = y_complex;
+  ca.I0 = I0;
+  ca.i0_stride = k;
+  ca.q = (int)k;
+  ca.sweeps = sweeps;
+  ca.cap = cap;
+  ca.qp = (int)(k | 1);
+  ca.tol = tol;
+  ca.tau = tau;
+  ca.I = I;
+  ca.J = J;
+  ca.stats = stats;
+  ca.status = status;
+  int cs = 0;
+  cudaError_t e = launch_ca(ca, nb, W->m > W->n ? W->m : W->n, st, &cs, &h->prof);
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(LRA_EUNSUPPORTED, "block %lld x %lld exceeds the cluster-shared-memory tier",
+                (long long)(W->m > W->n ? W->m : W->n), (long long)k);
+  CK(e);
+  h->launches += 1;
+  NucArgs na{};
+  na.op = ca.op;
+  na.w_stride = w_stride;
+  na.I = I;
+  na.J = J;
+  na.k = (int)k;
+  na.l = (int)k;
+  na.r = (int)r;
+  na.U = U;
+  na.TS = TS;
+  na.Sr = Sr;
+  na.status = status;
+  FacArgs fa{};
+  fa.op = ca.op;
+  fa.w_stride = w_stride;
+  fa.I = I;
+  fa.J = J;
+  fa.k = (int)k;
+  fa.l = (int)k;
+  fa.r = (int)r;
+  fa.TS = TS;
+  fa.Sr = Sr;
+  fa.A = A;
+  fa.B = B;
+  fa.a_stride = a_stride;
+  fa.b_stride = b_stride;
+  fa.status = status;
+  int nl = 0;
+  CK(launch_nucleus(na, fa, nb, st, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy, int y_complex,
+                            const int64_t *I0, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
+                            double tie_slack, int32_t swap_cap, int64_t *I, int64_t *J, double *U, double *A,
+                            double *B, lra_ca_stats *stats, void *stream) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  if ((s = check_operand(W)) != LRA_OK) return s;
+  if ((s = check_ca_shape(W, r, k, l, sweeps)) != LRA_OK) return s;
+  if (!Y && !I0) return fail(LRA_EINVAL, "need a sketch Y or a start set I0");
+  if (Y && ldy < W->m) return fail(LRA_EINVAL, "ldy < m");
+  if (!I || !J || !A || !B) return fail(LRA_EINVAL, "null output");
+  if (!(swap_tol >= 0.0) || !(tie_slack >= 0.0) || tie_slack >= 1.0 || swap_cap < 0)
+    return fail(LRA_EINVAL, "bad swap_tol / tie_slack / swap_cap");
+  Carve cv{nullptr, 0};
+  size_t need = 0;
+  {
+    Carve probe{nullptr, 0};
+    probe.take<int32_t>(1);
+    probe.take<double>((size_t)k * r);
+    probe.take<double>((size_t)k * r);
+    need = probe.off + 256;
+  }
+  if ((s = ws_reserve(h, need)) != LRA_OK) return s;
+  cv.base = (char *)h->ws;
+  int32_t *status = cv.take<int32_t>(1);
+  double *TS = cv.take<double>((size_t)k * r);
+  double *Sr = cv.take<double>((size_t)k * r);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+  s = run_chain(h, W, 0, Y, ldy, 0, y_complex, I0, r, k, sweeps, swap_tol, tie_slack, swap_cap, I, J, U, A, B, 0,
+                0, stats, status, TS, Sr, 1, st);
+  return s;
+}
+
+lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A, const double *B, int64_t r,
+                            int32_t prec, int64_t nsamples, const int64_t *si, const int64_t *sj, double *num2,
+                            double *den2, void *stream) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  if ((s = check_operand(W)) != LRA_OK) return s;
+  if (prec != LRA_RECON_PRECISE) return fail(LRA_EUNSUPPORTED, "only LRA_RECON_PRECISE is in this build");
+  if (!A || !B || !num2 || !den2 || r < 1) return fail(LRA_EINVAL, "null A/B/num2/den2 or r < 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nsamples > 0) {
+    if (!si || !sj) return fail(LRA_EINVAL, "sampled residual needs si, sj");
+    const int nblk = 296;
+    if ((s = ws_reserve(h, (size_t)2 * nblk * sizeof(double2) + 256)) != LRA_OK) return s;
+    int nl = 0;
+    CK(launch_sampled(make_view(W), A, B, (int)r, si, sj, nsamples, (double2 *)h->ws, nblk, num2, den2, st, &nl, &h->prof));
+    h->launches += nl;
+    return LRA_OK;
+  }
+  if (W->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "the full pass needs a dense operand (use nsamples > 0)");
+  const int64_t tiles = ((W->m + 127) / 128) * ((W->n + 127) / 128);
+  if ((s = ws_reserve(h, (size_t)tiles * sizeof(double2) + 256)) != LRA_OK) return s;
+  ResArgs a{};
+  a.dtype = W->dtype;
+  a.m = W->m;
+  a.n = W->n;
+  a.ldw = W->ldw;
+  a.w = W->w;
+  a.A = A;
+  a.B = B;
+  a.r = (int)r;
+  a.partial = (double2 *)h->ws;
+  a.status = nullptr;
+  int nl = 0;
+  CK(launch_residual(a, 1, num2, den2, st, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_stride, const lra_multiplier *M0,
+                     int64_t m_stride, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
+                     double tie_slack, int32_t swap_cap, int32_t prec, int64_t *I, int64_t *J, double *U,
+                     double *num2, double *den2, lra_ca_stats *stats, void *stream) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  if ((s = check_operand(W0)) != LRA_OK) return s;
+  if (W0->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "lra_batch needs dense blocks");
+  if (nb < 1) return fail(LRA_EINVAL, "nb >= 1");
+  if (w_stride < W0->ldw * W0->n) return fail(LRA_EINVAL, "w_stride < ldw*n (blocks overlap)");
+  if ((s = check_ca_shape(W0, r, k, l, sweeps)) != LRA_OK) return s;
+  if ((s = check_mult(M0, W0->n)) != LRA_OK) return s;
+  if (M0->lbar != k) return fail(LRA_EINVAL, "v1 requires lbar == k (reading C9)");
+  if (m_stride != 0 && M0->kind != LRA_MUL_SPARSE_PM1)
+    return fail(LRA_EINVAL, "per-block multipliers (m_stride != 0) are supported for SPARSE_PM1 only");
+  if (prec != LRA_RECON_PRECISE) return fail(LRA_EUNSUPPORTED, "only LRA_RECON_PRECISE is in this build");
+  if (!I || !J || !num2 || !den2) return fail(LRA_EINVAL, "null output");
+  const int64_t m = W0->m, n = W0->n;
+  const bool cplx = M0->kind == LRA_MUL_ARFT;
+  const size_t esz = cplx ? 16 : 8;
+  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  Carve probe{nullptr, 0};
+  probe.take<int32_t>(nb);
+  probe.take<char>((size_t)nb * m * k * esz);
+  probe.take<double>((size_t)nb * k * r);
+  probe.take<double>((size_t)nb * k * r);
+  probe.take<double>((size_t)nb * m * r);
+  probe.take<double>((size_t)nb * r * n);
+  probe.take<double2>((size_t)nb * tiles);
+  if ((s = ws_reserve(h, probe.off + 256)) != LRA_OK) return s;
+  Carve cv{(char *)h->ws, 0};
+  int32_t *status = cv.take<int32_t>(nb);
+  void *Y = cv.take<char>((size_t)nb * m * k * esz);
+  double *TS = cv.take<double>((size_t)nb * k * r);
+  double *Sr = cv.take<double>((size_t)nb * k * r);
+  double *A = cv.take<double>((size_t)nb * m * r);
+  double *B = cv.take<double>((size_t)nb * r * n);
+  double2 *part = cv.take<double2>((size_t)nb * tiles);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, st));
+  // stage 1 for all blocks
+  SketchArgs sa = make_sketch(W0, M0, Y, m);
+  sa.w_stride = w_stride;
+  sa.m_stride = m_stride;
+  sa.y_stride = m * k;
+  if (M0->kind == LRA_MUL_GAUSSIAN) sa.m_stride = 0;
+  CK(launch_sketch(sa, nb, M0->omega, M0->ld_omega, st, &h->prof));
+  h->launches += 1;
+  // stages 2-3, nucleus, factors
+  s = run_chain(h, W0, w_stride, Y, m, m * k, cplx ? 1 : 0, nullptr, r, k, sweeps, swap_tol, tie_slack, swap_cap, I,
+                J, U, A, B, m * r, r * n, stats, status, TS, Sr, nb, st);
+  if (s != LRA_OK) return s;
+  // a-posteriori check per block
+  ResArgs ra{};
+  ra.dtype = W0->dtype;
+  ra.m = m;
+  ra.n = n;
+  ra.ldw = W0->ldw;
+  ra.w_stride = w_stride;
+  ra.w = W0->w;
+  ra.A = A;
+  ra.B = B;
+  ra.a_stride = m * r;
+  ra.b_stride = r * n;
+  ra.r = (int)r;
+  ra.partial = part;
+  ra.status = status;
+  int nl = 0;
+  CK(launch_residual(ra, nb, num2, den2, st, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+// nucleus.cu — canonical nucleus (Alg 3.1 "algcnnncl") and the rank-r
+// factors of CUR = A*B.
+//
+// k_nucleus: one CTA per problem.  G = W[I,J] (k x l) is gathered to shared memory and
+// its SVD G = S Sigma T^T computed by one-sided (Hestenes) Jacobi in fp64 with a parallel
+// round-robin pair ordering (one warp per column pair).  Then
+//   U  = T_r Sigma_r^{-1} S_r^T                (l x k)  -> caller
+//   TS = T_r Sigma_r^{-1}  (l x r),  Sr = S_r  (k x r)  -> scratch for the factor kernels
+// k_factor_A: A = W[:,J] * TS  (m x r),   k_factor_B: B = Sr^T * W[I,:]  (r x n).
+#include "kernels.cuh"
+
+namespace lra {
+
+constexpr int NUC_NT = 256;
+constexpr int NUC_W = NUC_NT / 32;
+
+
+__device__ __forceinline__ void rr_pair(int L, int round, int i, int &a, int &b) {
+  // circle method on L (even) players: player 0 fixed, 1..L-1 rotate
+  if (i == 0) {
+    a = 0;
+    b = 1 + round % (L - 1);
+  } else {
+    a = 1 + (round + i) % (L - 1);
+    b = 1 + (round - i + (L - 1)) % (L - 1);
+  }
+}
+
+__global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
+  extern __shared__ __align__(16) double nsm[];
+  const int64_t b = blockIdx.x;
+  if (a.status[b] != LRA_OK) return;
+  const int k = a.k, l = a.l, r = a.r;
+  const int L = (l + 1) & ~1;          // even number of columns (zero pad)
+  const int ldg = k;                   // G column stride
+  double *G = nsm;                     // L columns of length k
+  double *V = G + (size_t)L * ldg;     // L x L
+  double *sig = V + (size_t)L * L;     // L
+  int *ord = reinterpret_cast<int *>(sig + L);
+  __shared__ int s_rot;
+  OpView op = a.op;
+  if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
+  const int64_t *I = a.I + b * k, *J = a.J + b * l;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < L * k; e += NUC_NT) {
+    int j = e / k, i = e % k;
+    G[e] = j < l ? op.at(I[i], J[j]) : 0.0;
+  }
+  for (int e = tid; e < L * L; e += NUC_NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
+  __syncthreads();
+  const double eps = 1e-15;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    int rot = 0;
+    for (int round = 0; round < L - 1; ++round) {
+      for (int pi = warp; pi < L / 2; pi += NUC_W) {
+        int p, qq;
+        rr_pair(L, round, pi, p, qq);
+        double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < k; i += 32) {
+          al = fma(gp[i], gp[i], al);
+          be = fma(gq[i], gq[i], be);
+          ga = fma(gp[i], gq[i], ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (fabs(ga) > eps * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < k; i += 32) {
+            double x = gp[i], y = gq[i];
+            gp[i] = cs * x - sn * y;
+            gq[i] = sn * x + cs * y;
+          }
+          double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
+          for (int i = lane; i < L; i += 32) {
+            double x = vp[i], y = vq[i];
+            vp[i] = cs * x - sn * y;
+            vq[i] = sn * x + cs * y;
+          }
+          rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (rot && lane == 0) atomicOr(&s_rot, 1);
+    __syncthreads();
+    if (!s_rot) break;
+  }
+  // singular values, descending order (ties: lower column first)
+  for (int j = warp; j < L; j += NUC_W) {
+    double s = 0.0;
+    for (int i = lane; i < k; i += 32) s = fma(G[(size_t)j * ldg + i], G[(size_t)j * ldg + i], s);
+    s = warp_sum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < L; ++j) ord[j] = j;
+    for (int x = 1; x < L; ++x) {   // insertion sort, stable
+      int v = ord[x];
+      int y = x - 1;
+      while (y >= 0 && sig[ord[y]] < sig[v]) { ord[y + 1] = ord[y]; --y; }
+      ord[y + 1] = v;
+    }
+    if (!(sig[ord[r - 1]] > 0.0) || !isfinite(sig[ord[0]])) a.status[b] = LRA_ESINGULAR;
+  }
+  __syncthreads();
+  if (a.status[b] != LRA_OK) return;
+  double *TS = a.TS + b * (int64_t)l * r, *Sr = a.Sr + b * (int64_t)k * r;
+  for (int e = tid; e < l * r; e += NUC_NT) {      // TS[j, t] = T[j, ord t] / sigma
+    int t = e / l, j = e % l;
+    int c = ord[t];
+    TS[(size_t)t * l + j] = V[(size_t)c * L + j] / sig[c];
+  }
+  for (int e = tid; e < k * r; e += NUC_NT) {      // Sr[i, t] = G[i, ord t] / sigma
+    int t = e / k, i = e % k;
+    int c = ord[t];
+    Sr[(size_t)t * k + i] = G[(size_t)c * ldg + i] / sig[c];
+  }
+  __syncthreads();
+  if (a.U) {
+    double *U = a.U + b * (int64_t)l * k;
+    for (int e = tid; e < l * k; e += NUC_NT) {    // U (l x k, col-major) = TS * Sr^T
+      int col = e / l, row = e % l;
+      double s = 0.0;
+      for (int t = 0; t < r; ++t) s = fma(TS[(size_t)t * l + row], Sr[(size_t)t * k + col], s);
+      U[(size_t)col * l + row] = s;
+    }
+  }
+}
+
+size_t nucleus_smem(int k, int l) {
+  int L = (l + 1) & ~1;
+  return ((size_t)L * k + (size_t)L * L + L) * 8 + (size_t)L * 4 + 16;
+}
+
+// ---------------------------------------------------------------------- factors
+
+// A = W[:,J] * TS.  grid (ceil(m/64), nb), 256 threads = 64 rows x 4 chunks of 16 outputs
+__global__ void __launch_bounds__(256) k_factor_A(FacArgs a) {
+  __shared__ double ts[LRA_QMAX * LRA_QMAX];
+  const int64_t b = blockIdx.y;
+  if (a.status[b] != LRA_OK) return;
+  OpView op = a.op;
+  if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
+  const int l = a.l, r = a.r;
+  const double *TS = a.TS + b * (int64_t)l * r;
+  for (int e = threadIdx.x; e < l * r; e += 256) ts[e] = TS[e];   // ts[t*l + j]
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * 64 + (threadIdx.x & 63);
+  const int chunk = threadIdx.x >> 6;
+  if (i >= op.m || chunk * 16 >= r) return;
+  const int64_t *J = a.J + b * l;
+  double acc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+  for (int j = 0; j < l; ++j) {
+    const double w = op.at(i, J[j]);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      int t = chunk * 16 + u;
+      if (t < r) acc[u] = fma(w, ts[t * l + j], acc[u]);
+    }
+  }
+  double *A = a.A + b * a.a_stride;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    int t = chunk * 16 + u;
+    if (t < r) A[(int64_t)t * op.m + i] = acc[u];
+  }
+}
+
+// B = Sr^T * W[I,:].  grid (ceil(n/64), nb), 256 threads = 64 columns x 4 chunks
+__global__ void __launch_bounds__(256) k_factor_B(FacArgs a) {
+  __shared__ double sr[LRA_QMAX * LRA_QMAX];
+  const int64_t b = blockIdx.y;
+  if (a.status[b] != LRA_OK) return;
+  OpView op = a.op;
+  if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
+  const int k = a.k, r = a.r;
+  const double *Sr = a.Sr + b * (int64_t)k * r;
+  for (int e = threadIdx.x; e < k * r; e += 256) sr[e] = Sr[e];   // sr[t*k + s]
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * 64 + (threadIdx.x & 63);
+  const int chunk = threadIdx.x >> 6;
+  if (j >= op.n || chunk * 16 >= r) return;
+  const int64_t *I = a.I + b * k;
+  double acc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+  for (int s = 0; s < k; ++s) {
+    const double w = op.at(I[s], j);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      int t = chunk * 16 + u;
+      if (t < r) acc[u] = fma(sr[t * k + s], w, acc[u]);
+    }
+  }
+  double *B = a.B + b * a.b_stride;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    int t = chunk * 16 + u;
+    if (t < r) B[j * r + t] = acc[u];
+  }
+}
+
+cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf) {
+  const size_t smem = nucleus_smem(na.k, na.l);
+  cudaError_t e = cudaFuncSetAttribute(k_nucleus, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  pf->begin("k_nucleus", st);
+  k_nucleus<<<(unsigned)nb, NUC_NT, smem, st>>>(na);
+  pf->end(st);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  dim3 gA((unsigned)((fa.op.m + 63) / 64), (unsigned)nb);
+  pf->begin("k_factor_A", st);
+  k_factor_A<<<gA, 256, 0, st>>>(fa);
+  pf->end(st);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  dim3 gB((unsigned)((fa.op.n + 63) / 64), (unsigned)nb);
+  pf->begin("k_factor_B", st);
+  k_factor_B<<<gB, 256, 0, st>>>(fa);
+  pf->end(st);
+  *nlaunch += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace lra

@@ -1,0 +1,290 @@
+// residual.cu — the a-posteriori check rho = ||W - CUR||_F / ||W||_F (eq. eqcur0,
+// P:1153-1155) with CUR = A*B, A m x r, B r x n (fp64).
+//
+// k_residual: one CTA per 128 x 128 tile of W (column-major).  The rank-r product is
+// accumulated in fp64 registers (8 x 8 per thread, DFMA) from A/B panels staged in shared
+// memory 16 k-columns at a time (A and B stay L2-resident across tiles); the epilogue
+// streams the W tile once with 16-byte loads, forms d = W - AB and accumulates sum d^2
+// and sum W^2 in fp64.  Per-tile partials are summed in a fixed order by k_reduce, so the
+// result is deterministic.  (PRECISE mode; the tensor-core FAST mode is not in this build.)
+#include "kernels.cuh"
+
+namespace lra {
+
+constexpr int RS_T = 128;    // tile edge
+constexpr int RS_KC = 16;    // k-chunk
+constexpr int RS_NT = 256;
+
+
+template <typename TW>
+__device__ __forceinline__ void ld8(const TW *p, bool vec, int rows_left, double v[8]);
+template <>
+__device__ __forceinline__ void ld8<float>(const float *p, bool vec, int rows_left, double v[8]) {
+  if (vec && rows_left >= 8) {
+    float4 a = __ldcs(reinterpret_cast<const float4 *>(p));
+    float4 b = __ldcs(reinterpret_cast<const float4 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int x = 0; x < 8; ++x) v[x] = x < rows_left ? (double)p[x] : 0.0;
+  }
+}
+template <>
+__device__ __forceinline__ void ld8<double>(const double *p, bool vec, int rows_left, double v[8]) {
+  if (vec && rows_left >= 8) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      double2 a = __ldcs(reinterpret_cast<const double2 *>(p) + x);
+      v[2 * x] = a.x; v[2 * x + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int x = 0; x < 8; ++x) v[x] = x < rows_left ? p[x] : 0.0;
+  }
+}
+
+// grid: (tiles_m * tiles_n, nb)
+template <typename TW>
+__global__ void __launch_bounds__(RS_NT) k_residual(ResArgs a) {
+  __shared__ __align__(16) double As[RS_KC][RS_T];
+  __shared__ __align__(16) double Bs[RS_KC][RS_T];
+  __shared__ double red[2][RS_NT / 32];
+  const int64_t b = blockIdx.y;
+  const int64_t tile = blockIdx.x;
+  if (a.status && a.status[b] != LRA_OK) return;
+  const int64_t tm = tile % a.tiles_m, tn = tile / a.tiles_m;
+  const int64_t row0 = tm * RS_T, col0 = tn * RS_T;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const double *A = a.A + b * a.a_stride;
+  const double *B = a.B + b * a.b_stride;
+  const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
+  double acc[8][8];
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y] = 0.0;
+  for (int k0 = 0; k0 < a.r; k0 += RS_KC) {
+    for (int e = tid; e < RS_KC * RS_T; e += RS_NT) {
+      int kk = e / RS_T, i = e % RS_T;
+      int64_t gi = row0 + i;
+      As[kk][i] = (k0 + kk < a.r && gi < a.m) ? A[(int64_t)(k0 + kk) * a.m + gi] : 0.0;
+    }
+    for (int e = tid; e < RS_KC * RS_T; e += RS_NT) {
+      int j = e / RS_KC, kk = e % RS_KC;
+      int64_t gj = col0 + j;
+      Bs[kk][j] = (k0 + kk < a.r && gj < a.n) ? B[gj * a.r + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < RS_KC; ++kk) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        double2 t = reinterpret_cast<const double2 *>(&As[kk][tx * 8])[x];
+        av[2 * x] = t.x; av[2 * x + 1] = t.y;
+        double2 u = reinterpret_cast<const double2 *>(&Bs[kk][ty * 8])[x];
+        bv[2 * x] = u.x; bv[2 * x + 1] = u.y;
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+  // epilogue: stream the W tile once
+  const int64_t gi0 = row0 + tx * 8;
+  const int rows_left = (int)max((int64_t)0, min((int64_t)8, a.m - gi0));
+  const bool vec = ((a.ldw & 7) == 0) && ((reinterpret_cast<uintptr_t>(W) & 31) == 0);
+  double num = 0.0, den = 0.0;
+#pragma unroll
+  for (int y = 0; y < 8; ++y) {
+    const int64_t gj = col0 + ty * 8 + y;
+    if (gj < a.n && rows_left > 0) {
+      double wv[8];
+      ld8<TW>(W + gj * a.ldw + gi0, vec, rows_left, wv);
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        if (x < rows_left) {
+          const double d = wv[x] - acc[x][y];
+          num = fma(d, d, num);
+          den = fma(wv[x], wv[x], den);
+        }
+      }
+    }
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = num;
+    red[1][tid >> 5] = den;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < RS_NT / 32; ++w) { s0 += red[0][w]; s1 += red[1][w]; }
+    a.partial[b * a.tiles_m * a.tiles_n + tile] = make_double2(s0, s1);
+  }
+}
+
+// per problem: fixed-order sum of its tile partials -> num2[b], den2[b]
+__global__ void __launch_bounds__(256) k_reduce(const double2 *partial, int64_t ntiles, double *num2,
+                                                double *den2, double scale_num, const int32_t *status) {
+  __shared__ double r0[8], r1[8];
+  const int64_t b = blockIdx.x;
+  if (status && status[b] != LRA_OK) {
+    if (threadIdx.x == 0) { num2[b] = NAN; den2[b] = NAN; }
+    return;
+  }
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t t = threadIdx.x; t < ntiles; t += 256) {
+    double2 p = partial[b * ntiles + t];
+    s0 += p.x;
+    s1 += p.y;
+  }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = s0; r1[threadIdx.x >> 5] = s1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < 8; ++w) { x += r0[w]; y += r1[w]; }
+    num2[b] = x * scale_num;
+    den2[b] = y;
+  }
+}
+
+cudaError_t launch_residual(ResArgs a, int64_t nb, double *num2, double *den2, cudaStream_t st, int *nlaunch, Prof *pf) {
+  a.tiles_m = (a.m + RS_T - 1) / RS_T;
+  a.tiles_n = (a.n + RS_T - 1) / RS_T;
+  dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)nb);
+  pf->begin("k_residual", st);
+  if (a.dtype == LRA_F32) k_residual<float><<<grid, RS_NT, 0, st>>>(a);
+  else k_residual<double><<<grid, RS_NT, 0, st>>>(a);
+  pf->end(st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  pf->begin("k_reduce", st);
+  k_reduce<<<(unsigned)nb, 256, 0, st>>>(a.partial, a.tiles_m * a.tiles_n, num2, den2, 1.0, a.status);
+  pf->end(st);
+  *nlaunch += 2;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- sampled residual
+// d_q = W(i_q, j_q) - A[i_q,:] B[:,j_q]; per-CTA partials of sum d^2.
+__global__ void __launch_bounds__(256) k_sampled(OpView op, const double *A, const double *B, int r,
+                                                 const int64_t *si, const int64_t *sj, int64_t Q,
+                                                 double2 *partial) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t q = (int64_t)blockIdx.x * 256 + threadIdx.x; q < Q; q += (int64_t)gridDim.x * 256) {
+    const int64_t i = si[q], j = sj[q];
+    double ab = 0.0;
+    for (int t = 0; t < r; ++t) ab = fma(A[(int64_t)t * op.m + i], B[j * r + t], ab);
+    const double d = op.at(i, j) - ab;
+    s = fma(d, d, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < 8; ++w) x += red[w];
+    partial[blockIdx.x] = make_double2(x, 0.0);
+  }
+}
+
+// dense ||W||_F^2 (per-CTA partials over column ranges)
+template <typename TW>
+__global__ void __launch_bounds__(256) k_sumsq(const TW *W, int64_t m, int64_t n, int64_t ldw, double2 *partial) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x)
+    for (int64_t i = threadIdx.x; i < m; i += 256) {
+      double w = (double)W[j * ldw + i];
+      s = fma(w, w, s);
+    }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < 8; ++w) x += red[w];
+    partial[blockIdx.x] = make_double2(0.0, x);
+  }
+}
+
+// factored ||W||_F^2 = tr((A^T A)(B B^T)) + 2 sum_E E.(AB) + sum E^2 (one CTA per row
+// block for the E terms; the Gram trace is computed by CTA 0 from the p x p Grams).
+__global__ void __launch_bounds__(256) k_fact_den(FactOp f, int64_t n, double2 *partial) {
+  __shared__ double red[8];
+  double s = 0.0;
+  // E terms over rows
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < f.m; i += (int64_t)gridDim.x * 256) {
+    for (int64_t e = f.rowptr[i]; e < f.rowptr[i + 1]; ++e) {
+      const int64_t j = f.col[e];
+      double ab = 0.0;
+      for (int64_t t = 0; t < f.p; ++t) ab = fma(f.fa[t * f.m + i], f.fb[j * f.p + t], ab);
+      const double v = f.val[e];
+      s += 2.0 * v * ab + v * v;
+    }
+  }
+  // Gram trace: CTA-strided over (t, u) pairs, each sum over rows / columns
+  for (int64_t tu = blockIdx.x; tu < f.p * f.p; tu += gridDim.x) {
+    const int64_t t = tu / f.p, u = tu % f.p;
+    double ga = 0.0, gb = 0.0;
+    for (int64_t i = threadIdx.x; i < f.m; i += 256) ga = fma(f.fa[t * f.m + i], f.fa[u * f.m + i], ga);
+    for (int64_t j = threadIdx.x; j < n; j += 256) gb = fma(f.fb[j * f.p + t], f.fb[j * f.p + u], gb);
+    ga = warp_sum(ga);
+    gb = warp_sum(gb);
+    __shared__ double ra[8], rb[8];
+    if ((threadIdx.x & 31) == 0) { ra[threadIdx.x >> 5] = ga; rb[threadIdx.x >> 5] = gb; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x = 0.0, y = 0.0;
+      for (int w = 0; w < 8; ++w) { x += ra[w]; y += rb[w]; }
+      s += x * y;
+    }
+    __syncthreads();
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int w = 0; w < 8; ++w) x += red[w];
+    partial[blockIdx.x] = make_double2(0.0, x);
+  }
+}
+
+cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,
+                           const int64_t *sj, int64_t Q, double2 *partial, int nblk, double *num2,
+                           double *den2, cudaStream_t st, int *nlaunch, Prof *pf) {
+  // partial layout: [0, nblk) sample partials, [nblk, 2 nblk) den partials
+  pf->begin("k_sampled", st);
+  k_sampled<<<nblk, 256, 0, st>>>(op, A, B, r, si, sj, Q, partial);
+  pf->end(st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  pf->begin("k_sumsq", st);
+  if (op.kind == LRA_OP_DENSE) {
+    if (op.dtype == LRA_F32)
+      k_sumsq<float><<<nblk, 256, 0, st>>>((const float *)op.w, op.m, op.n, op.ldw, partial + nblk);
+    else
+      k_sumsq<double><<<nblk, 256, 0, st>>>((const double *)op.w, op.m, op.n, op.ldw, partial + nblk);
+  } else {
+    k_fact_den<<<nblk, 256, 0, st>>>(op.f, op.n, partial + nblk);
+  }
+  pf->end(st);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // both halves reduce in one fixed-order pass: num from .x of the first half, den from .y
+  pf->begin("k_reduce", st);
+  k_reduce<<<1, 256, 0, st>>>(partial, 2 * (int64_t)nblk, num2, den2,
+                              (double)op.m * (double)op.n / (double)Q, nullptr);
+  pf->end(st);
+  *nlaunch += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace lra

@@ -1,0 +1,217 @@
+// sketch.cu — stage 1 of Alg 10.2: Y = W * M for the abridged randomized
+// Hadamard / Fourier multipliers, the sparse +-1 multiplier
+// and the dense Gaussian reference.
+//
+// W is column-major, so column c of Y is a signed (twiddled) sum of whole columns of W:
+//   ARHT: k_t = (sigma mod s) + t*s,      coef = D[k_t] * (-1)^popcount(t & floor(sigma/s))
+//   ARFT: k_t = 2^d (sigma mod s) + t,    coef = D[k_t] * omega_n^{t*sigma mod n}
+//   SPARSE_PM1: k_t = sp_row[c*nnz+t],    coef = sp_sign[c*nnz+t]
+// summed in ascending t with fp64 accumulation (one multiply, one add: bit-identical to
+// the oracle, reading C23).  Each CTA streams 2^d (or nnz) columns over a 1024-row tile
+// with 16-byte vector loads; the kernel is HBM-bound.
+#include "kernels.cuh"
+
+namespace lra {
+
+constexpr int SK_NT = 256;
+constexpr int SK_ROWS = SK_NT * 4;  // rows per CTA
+constexpr int SK_MAXT = 64;         // max terms per output column (2^d <= 64, nnz <= 64)
+
+
+template <typename TW>
+__device__ __forceinline__ void load4(const TW *p, bool vec, int64_t rows_left, double v[4]);
+
+template <>
+__device__ __forceinline__ void load4<float>(const float *p, bool vec, int64_t rows_left, double v[4]) {
+  if (vec && rows_left >= 4) {
+    float4 f = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) v[a] = a < rows_left ? (double)__ldg(p + a) : 0.0;
+  }
+}
+template <>
+__device__ __forceinline__ void load4<double>(const double *p, bool vec, int64_t rows_left, double v[4]) {
+  if (vec && rows_left >= 4) {
+    double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) v[a] = a < rows_left ? __ldg(p + a) : 0.0;
+  }
+}
+
+// grid: (row tiles, lbar, nb)
+template <typename TW, bool CPLX>
+__global__ void __launch_bounds__(SK_NT) k_sketch_structured(SketchArgs a) {
+  __shared__ int64_t s_k[SK_MAXT];
+  __shared__ double s_cr[SK_MAXT], s_ci[SK_MAXT];
+  __shared__ int s_T;
+  const int c = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
+  const int8_t *dsign = a.dsign;   // ARHT/ARFT blocks share one multiplier
+  if (threadIdx.x == 0) {
+    int T;
+    if (a.kind == LRA_MUL_SPARSE_PM1) {
+      T = a.nnz;
+      for (int t = 0; t < T; ++t) {
+        s_k[t] = a.sp_row[b * a.m_stride + (int64_t)c * a.nnz + t];
+        s_cr[t] = (double)a.sp_sign[b * a.m_stride + (int64_t)c * a.nnz + t];
+        s_ci[t] = 0.0;
+      }
+    } else {
+      const int64_t sigma = a.col[c];
+      const int64_t q = (int64_t)1 << a.depth, s = a.n >> a.depth;
+      T = (int)q;
+      for (int64_t t = 0; t < q; ++t) {
+        if (a.kind == LRA_MUL_ARHT) {
+          int64_t k = (sigma % s) + t * s;                       // H_{2^d} (x) I_s
+          int par = __popcll((unsigned long long)(t & (sigma / s))) & 1;
+          s_k[t] = k;
+          s_cr[t] = (double)dsign[k] * (par ? -1.0 : 1.0);
+          s_ci[t] = 0.0;
+        } else {                                                 // ARFT closed form (reading C4)
+          int64_t k = q * (sigma % s) + t;
+          int64_t e = (t * sigma) % a.n;
+          double ang = (2.0 * M_PI * (double)e) / (double)a.n;
+          double sn, cs;
+          sincos(ang, &sn, &cs);
+          double dk = (double)dsign[k];
+          s_k[t] = k;
+          s_cr[t] = dk * cs;
+          s_ci[t] = dk * sn;
+        }
+      }
+    }
+    s_T = T;
+  }
+  __syncthreads();
+  const int T = s_T;
+  const int64_t i0 = (int64_t)blockIdx.x * SK_ROWS + (int64_t)threadIdx.x * 4;
+  if (i0 >= a.m) return;
+  const int64_t left = a.m - i0;
+  const bool vec = ((a.ldw & 3) == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
+  double accr[4] = {0.0, 0.0, 0.0, 0.0}, acci[4] = {0.0, 0.0, 0.0, 0.0};
+  // loads of up to 8 terms in flight before the ordered accumulation
+  for (int t0 = 0; t0 < T; t0 += 8) {
+    double v[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < T) load4<TW>(W + s_k[t0 + u] * a.ldw + i0, vec, left, v[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u < T) {
+        const double cr = s_cr[t0 + u];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) accr[r] = __dadd_rn(accr[r], __dmul_rn(cr, v[u][r]));
+        if (CPLX) {
+          const double ci = s_ci[t0 + u];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acci[r] = __dadd_rn(acci[r], __dmul_rn(v[u][r], ci));
+        }
+      }
+    }
+  }
+  if (CPLX) {
+    double2 *Y = reinterpret_cast<double2 *>(a.y) + b * a.y_stride + (int64_t)c * a.ldy;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (r < left) Y[i0 + r] = make_double2(accr[r], acci[r]);
+  } else {
+    double *Y = reinterpret_cast<double *>(a.y) + b * a.y_stride + (int64_t)c * a.ldy;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (r < left) Y[i0 + r] = accr[r];
+  }
+}
+
+// Dense Gaussian reference Y = W * Omega, accumulated sequentially in k (ascending) per
+// output in fp64.  When a K-chunk of Omega holds only fp32-representable values and W is
+// fp32, every product is exact and FMA equals multiply-then-add; otherwise the product is
+// rounded first (oracle order).  grid: (ceil(m/32), ceil(lbar/16), nb)
+constexpr int GS_R = 32, GS_C = 16, GS_K = 64;
+template <typename TW>
+__global__ void __launch_bounds__(128) k_sketch_gauss(SketchArgs a, const double *omega, int64_t ldo) {
+  __shared__ double Ws[GS_K][GS_R + 1];
+  __shared__ double Os[GS_K][GS_C];
+  __shared__ int s_exact;
+  const int64_t b = blockIdx.z;
+  const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
+  const int64_t r0 = (int64_t)blockIdx.x * GS_R, c0 = (int64_t)blockIdx.y * GS_C;
+  const int tid = threadIdx.x;
+  const int tr = tid % 16, tc = tid / 16;     // thread: rows tr, tr+16; cols tc, tc+8
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const bool wf32 = sizeof(TW) == 4;
+  for (int64_t k0 = 0; k0 < a.n; k0 += GS_K) {
+    int exact = 1;
+    for (int e = tid; e < GS_K * GS_R; e += 128) {
+      int kk = e / GS_R, rr = e % GS_R;
+      int64_t i = r0 + rr, k = k0 + kk;
+      Ws[kk][rr] = (i < a.m && k < a.n) ? (double)W[k * a.ldw + i] : 0.0;
+    }
+    for (int e = tid; e < GS_K * GS_C; e += 128) {
+      int kk = e / GS_C, cc = e % GS_C;
+      int64_t k = k0 + kk, c = c0 + cc;
+      double o = (k < a.n && c < a.lbar) ? omega[c * ldo + k] : 0.0;
+      Os[kk][cc] = o;
+      exact &= ((double)(float)o == o);
+    }
+    exact = __syncthreads_and(exact && wf32);
+    const int kmax = (int)min((int64_t)GS_K, a.n - k0);
+    if (exact) {
+      for (int kk = 0; kk < kmax; ++kk) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) acc[x][y] = fma(Ws[kk][tr + 16 * x], Os[kk][tc + 8 * y], acc[x][y]);
+      }
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y)
+            acc[x][y] = __dadd_rn(acc[x][y], __dmul_rn(Ws[kk][tr + 16 * x], Os[kk][tc + 8 * y]));
+      }
+    }
+    __syncthreads();
+  }
+  double *Y = reinterpret_cast<double *>(a.y) + b * a.y_stride;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      int64_t i = r0 + tr + 16 * x, c = c0 + tc + 8 * y;
+      if (i < a.m && c < a.lbar) Y[c * a.ldy + i] = acc[x][y];
+    }
+  (void)s_exact;
+}
+
+cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo,
+                          cudaStream_t st, Prof *pf) {
+  if (a.kind == LRA_MUL_GAUSSIAN) {
+    dim3 grid((unsigned)((a.m + GS_R - 1) / GS_R), (unsigned)((a.lbar + GS_C - 1) / GS_C), (unsigned)nb);
+    pf->begin("k_sketch_gauss", st);
+    if (a.dtype == LRA_F32) k_sketch_gauss<float><<<grid, 128, 0, st>>>(a, omega, ldo);
+    else k_sketch_gauss<double><<<grid, 128, 0, st>>>(a, omega, ldo);
+    pf->end(st);
+    return cudaGetLastError();
+  }
+  dim3 grid((unsigned)((a.m + SK_ROWS - 1) / SK_ROWS), (unsigned)a.lbar, (unsigned)nb);
+  const bool cplx = a.kind == LRA_MUL_ARFT;
+  pf->begin(a.kind == LRA_MUL_SPARSE_PM1 ? "k_sketch_sparse" : (cplx ? "k_sketch_arft" : "k_sketch_arht"), st);
+  if (a.dtype == LRA_F32) {
+    if (cplx) k_sketch_structured<float, true><<<grid, SK_NT, 0, st>>>(a);
+    else k_sketch_structured<float, false><<<grid, SK_NT, 0, st>>>(a);
+  } else {
+    if (cplx) k_sketch_structured<double, true><<<grid, SK_NT, 0, st>>>(a);
+    else k_sketch_structured<double, false><<<grid, SK_NT, 0, st>>>(a);
+  }
+  pf->end(st);
+  return cudaGetLastError();
+}
+
+}  // namespace lra

@@ -1,0 +1,261 @@
+"""Thin ctypes binding of liblra.so (include/lra.h): same names, argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; PyTorch only supplies device
+memory (tensors), the stream handle and, for multi-GPU runs, the process group.  There is
+no CPU fallback: if liblra.so is missing or no CUDA device is present, calls raise.
+
+Conventions: a dense m×n matrix W is a torch tensor ``Wt`` of shape (n, m), C-contiguous —
+i.e. W column-major with ldw = m (``to_colmajor`` converts a numpy (m, n) array).  Batches
+are (nb, n, m).  Index sets are int64 tensors, U is (k, l) storage of the l×k column-major
+nucleus, A is (r, m) storage of the m×r column-major factor, B is (n, r) storage of the
+r×n column-major factor.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liblra.so")
+
+LRA_OK, LRA_EINVAL, LRA_ESINGULAR, LRA_ENOMEM, LRA_ECUDA, LRA_ENCCL, LRA_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+LRA_F32, LRA_F64 = 0, 1
+LRA_OP_DENSE, LRA_OP_FACTORED_CSR = 0, 1
+LRA_MUL_NONE, LRA_MUL_GAUSSIAN, LRA_MUL_ARHT, LRA_MUL_ARFT, LRA_MUL_SPARSE_PM1 = 0, 1, 2, 3, 4
+LRA_RECON_FAST, LRA_RECON_PRECISE = 0, 1
+MUL_KIND = {"none": LRA_MUL_NONE, "gaussian": LRA_MUL_GAUSSIAN, "arht": LRA_MUL_ARHT,
+            "arft": LRA_MUL_ARFT, "sparse": LRA_MUL_SPARSE_PM1}
+
+
+class lra_operand(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dtype", C.c_int32), ("m", C.c_int64), ("n", C.c_int64),
+                ("w", C.c_void_p), ("ldw", C.c_int64), ("fa", C.c_void_p), ("fb", C.c_void_p),
+                ("p", C.c_int64), ("e_rowptr", C.c_void_p), ("e_col", C.c_void_p), ("e_val", C.c_void_p)]
+
+
+class lra_multiplier(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("depth", C.c_int32), ("lbar", C.c_int64), ("dsign", C.c_void_p),
+                ("col", C.c_void_p), ("sp_row", C.c_void_p), ("sp_sign", C.c_void_p),
+                ("nnz_per_col", C.c_int32), ("omega", C.c_void_p), ("ld_omega", C.c_int64)]
+
+
+STATS_DTYPE = np.dtype([("status", np.int32), ("loops_done", np.int32), ("lu_steps", np.int32),
+                        ("swaps", np.int32), ("cap_hits", np.int32), ("sketch_swaps", np.int32),
+                        ("cert_rows", np.float64), ("cert_cols", np.float64)])
+assert STATS_DTYPE.itemsize == 40
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+class LraError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"lra status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(_SO):
+        raise LibraryMissing(f"{_SO} not built — run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(_SO)
+    vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    P = C.POINTER
+    lib.lra_handle_create.argtypes = [P(vp), C.c_int, vp, C.c_int, C.c_int]
+    lib.lra_handle_destroy.argtypes = [vp]
+    lib.lra_handle_destroy.restype = None
+    lib.lra_preprocess.argtypes = [vp, P(lra_operand), P(lra_multiplier), vp, i64, vp]
+    lib.lra_cross_approx.argtypes = [vp, P(lra_operand), vp, i64, C.c_int, vp, i64, i64, i64, i32, dbl, dbl, i32,
+                                     vp, vp, vp, vp, vp, vp, vp]
+    lib.lra_cur_residual.argtypes = [vp, P(lra_operand), vp, vp, i64, i32, i64, vp, vp, vp, vp, vp]
+    lib.lra_batch.argtypes = [vp, i64, P(lra_operand), i64, P(lra_multiplier), i64, i64, i64, i64, i32, dbl, dbl,
+                              i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    lib.lra_last_error.restype = C.c_char_p
+    lib.lra_launch_count.argtypes = [vp]
+    lib.lra_launch_count.restype = i64
+    lib.lra_profile_enable.argtypes = [vp, C.c_int]
+    lib.lra_profile_enable.restype = C.c_int
+    lib.lra_profile_read.argtypes = [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(i64)]
+    lib.lra_profile_read.restype = C.c_int
+    for f in ("lra_handle_create", "lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
+        getattr(lib, f).restype = C.c_int
+    return lib
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
+
+
+EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
+            "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
+            "lra_profile_read"]
+
+
+def _check(st):
+    if st != LRA_OK:
+        raise LraError(st, lib().lra_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ marshalling helpers
+def to_colmajor(W_np, device="cuda"):
+    """numpy (m, n) → torch (n, m) contiguous on ``device`` (column-major W, same bits)."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(W_np).T)).to(device)
+
+
+class Dense:
+    """A dense operand: Wt is (n, m) [or (nb, n, m) for batches], fp32 or fp64."""
+
+    def __init__(self, Wt):
+        import torch
+        assert Wt.is_cuda and Wt.is_contiguous() and Wt.dtype in (torch.float32, torch.float64)
+        self.Wt = Wt
+        self.n, self.m = Wt.shape[-2], Wt.shape[-1]
+
+    def struct(self):
+        import torch
+        return lra_operand(LRA_OP_DENSE, LRA_F32 if self.Wt.dtype == torch.float32 else LRA_F64,
+                           self.m, self.n, self.Wt.data_ptr(), self.m, None, None, 0, None, None, None)
+
+    def block_stride(self):
+        return self.m * self.n
+
+
+class Factored:
+    """Entry oracle W = A·B + E (config 4): A (p, m) storage of m×p col-major fp64, B (n, p)
+    storage of p×n col-major fp64, CSR row_ptr (m+1), col, val on device."""
+
+    def __init__(self, A_t, B_t, row_ptr, col, val, m, n, p):
+        self.A_t, self.B_t, self.row_ptr, self.col, self.val = A_t, B_t, row_ptr, col, val
+        self.m, self.n, self.p = m, n, p
+
+    def struct(self):
+        return lra_operand(LRA_OP_FACTORED_CSR, LRA_F64, self.m, self.n, None, self.m, self.A_t.data_ptr(),
+                           self.B_t.data_ptr(), self.p, self.row_ptr.data_ptr(), self.col.data_ptr(),
+                           self.val.data_ptr())
+
+
+class Multiplier:
+    """Device copy of a realized multiplier (``synth.multiplier_*`` dict)."""
+
+    def __init__(self, mult: dict, device="cuda"):
+        import torch
+        self.mult = mult
+        self.kind = mult["kind"]
+        self.t = {}
+        for key in ("dsign", "col", "sp_row", "sp_sign"):
+            if key in mult:
+                self.t[key] = torch.from_numpy(np.ascontiguousarray(mult[key])).to(device)
+        if "omega" in mult:   # (lbar, n) storage of the n×lbar col-major matrix
+            self.t["omega"] = torch.from_numpy(np.ascontiguousarray(np.asarray(mult["omega"]).T)).to(device)
+        self.lbar = mult["lbar"]
+        self.n = mult["n"]
+
+    def struct(self):
+        om = self.t.get("omega")
+        return lra_multiplier(MUL_KIND[self.kind], int(self.mult.get("depth", 0)), self.lbar,
+                              _ptr(self.t.get("dsign")), _ptr(self.t.get("col")), _ptr(self.t.get("sp_row")),
+                              _ptr(self.t.get("sp_sign")), int(self.mult.get("nnz", 0)), _ptr(om),
+                              self.n if om is not None else 0)
+
+    def m_stride(self):
+        """Per-block stride for lra_batch: stacked sparse multipliers (synth.multiplier_sparse_batch)
+        advance by lbar·nnz entries per block; every other multiplier is shared (0)."""
+        if self.kind == "sparse" and "nb" in self.mult:
+            return self.lbar * int(self.mult["nnz"])
+        return 0
+
+
+# ------------------------------------------------------------------ the C-ABI, same names
+class Handle:
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        _check(lib().lra_handle_create(C.byref(h), int(device), None, 1, 0))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().lra_handle_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self):
+        return int(lib().lra_launch_count(self.h))
+
+    def profile(self, enable=True):
+        _check(lib().lra_profile_enable(self.h, int(bool(enable))))
+
+    def profile_read(self, cap=32):
+        """{kernel name: (total ms, launches)} since the last enable/read (synchronizes)."""
+        names = (C.c_char_p * cap)()
+        ms = (C.c_double * cap)()
+        cnt = (C.c_int64 * cap)()
+        nd = lib().lra_profile_read(self.h, cap, names, ms, cnt)
+        if nd < 0:
+            _check(nd)
+        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(nd)}
+
+
+def lra_handle_create(device=0):
+    return Handle(device)
+
+
+def lra_preprocess(h, W, M, Y, stream=None):
+    """Y (lbar, m) float64 [or (lbar, m, 2) for ARFT] receives Y = W·M (column-major)."""
+    ldy = Y.shape[1]
+    _check(lib().lra_preprocess(h.h, C.byref(W.struct()), C.byref(M.struct()), _ptr(Y), ldy, _stream(stream)))
+
+
+def lra_cross_approx(h, W, Y, I0, r, k, l, sweeps, I, J, U, A, B, stats=None, y_complex=False,
+                     swap_tol=1e-12, tie_slack=1e-12, swap_cap=None, stream=None):
+    ldy = Y.shape[1] if Y is not None else 0
+    cap = 20 * k if swap_cap is None else swap_cap
+    _check(lib().lra_cross_approx(h.h, C.byref(W.struct()), _ptr(Y), ldy, int(bool(y_complex)), _ptr(I0), r, k, l,
+                                  sweeps, swap_tol, tie_slack, cap, _ptr(I), _ptr(J), _ptr(U), _ptr(A), _ptr(B),
+                                  _ptr(stats), _stream(stream)))
+
+
+def lra_cur_residual(h, W, A, B, r, num2, den2, nsamples=0, si=None, sj=None, prec=LRA_RECON_PRECISE, stream=None):
+    _check(lib().lra_cur_residual(h.h, C.byref(W.struct()), _ptr(A), _ptr(B), r, prec, nsamples, _ptr(si), _ptr(sj),
+                                  _ptr(num2), _ptr(den2), _stream(stream)))
+
+
+def lra_batch(h, nb, W, M, r, k, l, sweeps, I, J, U, num2, den2, stats=None, swap_tol=1e-12, tie_slack=1e-12,
+              swap_cap=None, prec=LRA_RECON_PRECISE, stream=None):
+    cap = 20 * k if swap_cap is None else swap_cap
+    _check(lib().lra_batch(h.h, nb, C.byref(W.struct()), W.block_stride(), C.byref(M.struct()), M.m_stride(), r, k, l,
+                           sweeps, swap_tol, tie_slack, cap, prec, _ptr(I), _ptr(J), _ptr(U), _ptr(num2), _ptr(den2),
+                           _ptr(stats), _stream(stream)))
+
+
+def stats_to_numpy(stats_t):
+    """Device stats buffer (uint8 tensor of 40·nb bytes) → numpy structured array."""
+    return np.frombuffer(stats_t.cpu().numpy().tobytes(), dtype=STATS_DTYPE)
+
+
+def new_stats(nb=1, device="cuda"):
+    import torch
+    return torch.zeros(40 * nb, dtype=torch.uint8, device=device)

@@ -1,0 +1,62 @@
+"""End-to-end call sequence of the hot path through the C-ABI (user-facing convenience).
+
+``cur`` runs Alg 10.2 + C-A (stages 1–3), the canonical nucleus and the a-posteriori
+check on one dense matrix: lra_preprocess → lra_cross_approx → lra_cur_residual.
+``cur_batch`` runs ``lra_batch`` on nb same-shape blocks.  All work happens in liblra.so.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import lra as L
+
+
+class CurBuffers:
+    """Preallocated device outputs for one problem (reused across calls)."""
+
+    def __init__(self, m, n, r, k, cplx=False, device="cuda"):
+        f64 = dict(dtype=torch.float64, device=device)
+        self.Y = torch.empty((k, m, 2) if cplx else (k, m), **f64)
+        self.I = torch.empty(k, dtype=torch.int64, device=device)
+        self.J = torch.empty(k, dtype=torch.int64, device=device)
+        self.U = torch.empty((k, k), **f64)          # l×k column-major
+        self.A = torch.empty((r, m), **f64)          # m×r column-major
+        self.B = torch.empty((n, r), **f64)          # r×n column-major
+        self.num2 = torch.empty(1, **f64)
+        self.den2 = torch.empty(1, **f64)
+        self.stats = L.new_stats(1, device)
+
+
+def cur(h, W, M, r, k, sweeps, bufs=None, I0=None, swap_tol=1e-12, tie_slack=1e-12, stream=None):
+    """W: lra.Dense (or lra.Factored with M None and I0 given); M: lra.Multiplier or None."""
+    cplx = M is not None and M.kind == "arft"
+    if bufs is None:
+        bufs = CurBuffers(W.m, W.n, r, k, cplx)
+    if M is not None:
+        L.lra_preprocess(h, W, M, bufs.Y, stream=stream)
+        Y = bufs.Y
+    else:
+        Y = None
+    L.lra_cross_approx(h, W, Y, I0, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.A, bufs.B, bufs.stats,
+                       y_complex=cplx, swap_tol=swap_tol, tie_slack=tie_slack, stream=stream)
+    if isinstance(W, L.Dense):
+        L.lra_cur_residual(h, W, bufs.A, bufs.B, r, bufs.num2, bufs.den2, stream=stream)
+    return bufs
+
+
+class BatchBuffers:
+    def __init__(self, nb, r, k, device="cuda"):
+        self.I = torch.empty((nb, k), dtype=torch.int64, device=device)
+        self.J = torch.empty((nb, k), dtype=torch.int64, device=device)
+        self.U = torch.empty((nb, k, k), dtype=torch.float64, device=device)
+        self.num2 = torch.empty(nb, dtype=torch.float64, device=device)
+        self.den2 = torch.empty(nb, dtype=torch.float64, device=device)
+        self.stats = L.new_stats(nb, device)
+
+
+def cur_batch(h, W, M, r, k, sweeps, nb, bufs=None, swap_tol=1e-12, tie_slack=1e-12, stream=None):
+    if bufs is None:
+        bufs = BatchBuffers(nb, r, k)
+    L.lra_batch(h, nb, W, M, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2, bufs.stats,
+                swap_tol=swap_tol, tie_slack=tie_slack, stream=stream)
+    return bufs

@@ -1,0 +1,69 @@
+"""CPU-side checks of the boundary (no GPU compute): the C-ABI library loads, exports every
+symbol include/lra.h declares, the ctypes structs match the header's layout, and every
+entry point fails loudly (LRA_ECUDA) when no device is present — there is no CPU fallback."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_1710_07946_b200._build as B
+    B.build()
+    from paper_1710_07946_b200 import lra
+    return lra
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "lra.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lra_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    fns = _header_functions()
+    for f in ("lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(L):
+    lib = L.lib()
+    for f in _header_functions():
+        assert hasattr(lib, f), f"liblra.so does not export {f}"
+    assert set(L.EXPORTED) == set(_header_functions())
+
+
+def test_struct_layouts(L):
+    assert ctypes.sizeof(L.lra_operand) == 4 + 4 + 8 * 10
+    assert ctypes.sizeof(L.lra_multiplier) == 4 + 4 + 8 * 5 + 4 + 4 + 8 + 8
+    assert L.STATS_DTYPE.itemsize == 40
+
+
+def test_no_cpu_fallback(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(L.LraError) as e:
+        L.Handle(0)
+    assert e.value.status == L.LRA_ECUDA
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    from paper_1710_07946_b200 import lra
+    monkeypatch.setattr(lra, "_SO", str(tmp_path / "nope.so"))
+    monkeypatch.setattr(lra, "_lib", None)
+    with pytest.raises(lra.LibraryMissing):
+        lra.lib()
+
+
+def test_product_path_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1710_07946_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", txt, re.M), f

@@ -1,0 +1,219 @@
+"""GPU ↔ oracle parity through the C-ABI (liblra.so).  Needs a B200: marked ``gpu``.
+
+Tolerances (BASELINE.json): pivots (I, J in slot order) bit-exact; sketches
+bit-exact where both sides sum in the same order; fp64 mode |ρ_gpu − ρ_ora| ≤ 1e-12;
+fp32 mode |ρ_gpu/ρ_ora − 1| ≤ 1e-4; nucleus U to 1e-9 relative (different SVD codes)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import lra as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1710_07946_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def h(P):
+    return P.Handle(0)
+
+
+def _dense(P, W):
+    return P.lra.Dense(P.lra.to_colmajor(W))
+
+
+def _run_gpu(P, h, W, mult, r, k, sweeps, I0=None):
+    from paper_1710_07946_b200 import pipeline
+    Wd = _dense(P, W)
+    M = P.lra.Multiplier(mult) if mult is not None else None
+    I0t = torch.from_numpy(np.asarray(I0, np.int64)).cuda() if I0 is not None else None
+    bufs = pipeline.cur(h, Wd, M, r, k, sweeps, I0=I0t)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)[0]
+    return bufs, st
+
+
+def _y_numpy(bufs, cplx):
+    Y = bufs.Y.cpu().numpy()
+    if cplx:
+        return (Y[..., 0] + 1j * Y[..., 1]).T
+    return Y.T
+
+
+def _check_pipeline(P, h, W, mult, r, k, sweeps, rho_tol_abs=None, rho_tol_rel=None, y_exact=True, I0=None):
+    ora = O.cur_pipeline(W, mult, r, k, k, sweeps, I0=I0)
+    bufs, st = _run_gpu(P, h, W, mult, r, k, sweeps, I0=I0)
+    assert st["status"] == 0
+    if mult is not None:
+        Yg = _y_numpy(bufs, mult["kind"] == "arft")
+        if y_exact:
+            assert np.array_equal(Yg, ora.Y), "sketch not bit-identical"
+        else:
+            assert np.allclose(Yg, ora.Y, rtol=0, atol=1e-14 * np.abs(ora.Y).max())
+    assert list(bufs.I.cpu().numpy()) == list(ora.I), "row pivots differ"
+    assert list(bufs.J.cpu().numpy()) == list(ora.J), "column pivots differ"
+    assert st["loops_done"] == ora.ca.loops_done
+    assert st["swaps"] == ora.ca.swaps and st["lu_steps"] == ora.ca.lu_steps
+    U = bufs.U.cpu().numpy().T          # (k, l) storage → l×k
+    assert np.allclose(U, ora.U, rtol=1e-9, atol=1e-9 * np.abs(ora.U).max())
+    rho = float(np.sqrt(bufs.num2.item() / bufs.den2.item()))
+    if rho_tol_abs is not None:
+        assert abs(rho - ora.rho) <= rho_tol_abs, (rho, ora.rho)
+    if rho_tol_rel is not None:
+        assert abs(rho / ora.rho - 1) <= rho_tol_rel, (rho, ora.rho)
+    assert st["cert_rows"] <= 1 + 1e-12 and st["cert_cols"] <= 1 + 1e-12
+    return rho, ora
+
+
+# ------------------------------------------------------------------ configs
+def test_config1_fp64_exact_recovery(P, h):
+    """BASELINE config 1: fp64, ARHT d=3, k=l=r=8, 2 sweeps: pivots bit-exact,
+    |Δρ| ≤ 1e-12, ρ ≤ 1e-9, dominance ≤ 1+1e-12."""
+    W = synth.config1(0)
+    M = synth.multiplier_abridged(0, 256, 3, 8, "arht")
+    rho, ora = _check_pipeline(P, h, W, M, 8, 8, 2, rho_tol_abs=1e-12)
+    assert rho <= 1e-9
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_more_seeds(P, h, seed):
+    W = synth.config1(seed)
+    M = synth.multiplier_abridged(seed, 256, 3, 8, "arht")
+    _check_pipeline(P, h, W, M, 8, 8, 2, rho_tol_abs=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["arht", "arft", "gaussian"])
+def test_config2_full_size(P, h, kind):
+    """BASELINE config 2 at full size (4096², fp32, r=32, k=l=48, 3 sweeps)."""
+    W = synth.config2(0)
+    M = (synth.multiplier_gaussian(0, 4096, 48) if kind == "gaussian"
+         else synth.multiplier_abridged(0, 4096, 4, 48, kind))
+    _check_pipeline(P, h, W, M, 32, 48, 3, rho_tol_rel=1e-4, y_exact=(kind != "arft"))
+
+
+def test_config3_batch_vs_oracle(P, h):
+    """BASELINE config 3 recipe on a 48-block batch through lra_batch (sparse ±1, r=16,
+    k=l=20, 2 sweeps): every block's pivots equal the oracle's, ρ within 1e-4."""
+    from paper_1710_07946_b200 import pipeline
+    nb = 48
+    s, t = synth.cauchy_params(0, nb)
+    Wt = synth.cauchy_blocks_torch(s, t, "cuda")
+    Ms = synth.multiplier_sparse_batch(0, nb, 512, 20)
+    M = P.lra.Multiplier(Ms)
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), M, 16, 20, 2, nb)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)
+    for b in range(nb):
+        W = synth.cauchy_block(s[b], t[b])
+        assert np.array_equal(Wt[b].cpu().numpy().T, W)
+        Mb = dict(Ms, sp_row=Ms["sp_row"][b], sp_sign=Ms["sp_sign"][b])
+        ora = O.cur_pipeline(W, Mb, 16, 20, 20, 2)
+        assert st[b]["status"] == 0
+        assert list(bufs.I[b].cpu().numpy()) == list(ora.I)
+        assert list(bufs.J[b].cpu().numpy()) == list(ora.J)
+        rho = float(np.sqrt(bufs.num2[b].item() / bufs.den2[b].item()))
+        assert abs(rho / ora.rho - 1) <= 1e-4, (b, rho, ora.rho)
+
+
+# ------------------------------------------------------------------ ragged / edge cases
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("m,n,d,k,r", [(1000, 776, 3, 13, 9), (333, 520, 2, 7, 7), (130, 96, 5, 5, 3)])
+def test_ragged_shapes(P, h, dtype, m, n, d, k, r):
+    W = synth.factor_gaussian(m + n, m, n, r, 1e-14).astype(dtype)
+    M = synth.multiplier_abridged(7, n, d, k, "arht")
+    _check_pipeline(P, h, np.asfortranarray(W), M, r, k, 3, rho_tol_rel=1e-6)
+
+
+def test_random_start_no_multiplier(P, h):
+    """Tests 2 protocol: random I₀, no sketch."""
+    W = synth.factor_gaussian(3, 700, 500, 6, 1e-16)
+    I0 = synth.random_rows(3, 700, 6)
+    _check_pipeline(P, h, W, None, 6, 6, 4, rho_tol_rel=1e-6, I0=I0)
+
+
+@pytest.mark.parametrize("kind", ["arht", "arft", "sparse", "gaussian"])
+def test_preprocess_ragged_bit_exact(P, h, kind):
+    m, n = 1237, 96
+    W = np.asfortranarray(synth.factor_gaussian(11, m, n, 5, 1e-6).astype(np.float32))
+    if kind == "sparse":
+        mult = synth.multiplier_sparse(4, n, 9)
+    elif kind == "gaussian":
+        mult = synth.multiplier_gaussian(4, n, 9)
+    else:
+        mult = synth.multiplier_abridged(4, n, 5, 9, kind)
+    Y = torch.empty((9, m, 2) if kind == "arft" else (9, m), dtype=torch.float64, device="cuda")
+    P.lra_preprocess(h, _dense(P, W), P.lra.Multiplier(mult), Y)
+    torch.cuda.synchronize()
+    Yg = Y.cpu().numpy()
+    Yg = (Yg[..., 0] + 1j * Yg[..., 1]).T if kind == "arft" else Yg.T
+    ref = O.sketch(W, mult)
+    if kind == "arft":
+        assert np.allclose(Yg, ref, rtol=0, atol=1e-15 * np.abs(ref).max())
+    else:
+        assert np.array_equal(Yg, ref)
+
+
+def test_residual_given_oracle_factors(P, h):
+    """Stage-isolated a5: the GPU residual of the oracle's A, B equals the oracle's to 1e-12."""
+    W = synth.config1(5)
+    M = synth.multiplier_abridged(5, 256, 3, 8, "arht")
+    ora = O.cur_pipeline(W, M, 8, 8, 8, 2)
+    A = torch.from_numpy(np.ascontiguousarray(ora.A.T)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(ora.B.T)).cuda()
+    num2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    den2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.lra_cur_residual(h, _dense(P, W), A, B, 8, num2, den2)
+    torch.cuda.synchronize()
+    rho = np.sqrt(num2.item() / den2.item())
+    assert abs(rho - ora.rho) <= 1e-12
+    assert den2.item() == pytest.approx(ora.den2, rel=1e-14)
+
+
+def test_sampled_residual_matches_oracle(P, h):
+    W = synth.factor_gaussian(1, 300, 200, 4, 1e-4)
+    M = synth.multiplier_abridged(1, 200, 3, 4, "arht")
+    ora = O.cur_pipeline(W, M, 4, 4, 4, 2)
+    ii, jj = synth.sample_pairs(9, 300, 200, 100000)
+    est = O.sampled_residual(O.DenseOperand(W), ora.A, ora.B, ii, jj)
+    A = torch.from_numpy(np.ascontiguousarray(ora.A.T)).cuda()
+    B = torch.from_numpy(np.ascontiguousarray(ora.B.T)).cuda()
+    num2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    den2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.lra_cur_residual(h, _dense(P, W), A, B, 4, num2, den2, nsamples=len(ii),
+                       si=torch.from_numpy(ii).cuda(), sj=torch.from_numpy(jj).cuda())
+    torch.cuda.synchronize()
+    assert num2.item() == pytest.approx(est, rel=1e-10)
+    assert den2.item() == pytest.approx(ora.den2, rel=1e-13)
+
+
+def test_singular_generator_reported(P, h):
+    """±δ matrix (Example exdlt): the C-A sees only zeros → ESINGULAR in stats, not a crash."""
+    W = np.zeros((64, 64))
+    W[40, 33] = 1.0
+    from paper_1710_07946_b200 import pipeline
+    I0 = torch.tensor([0, 1], dtype=torch.int64, device="cuda")
+    bufs = pipeline.cur(h, _dense(P, W), None, 2, 2, 2, I0=I0)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)[0]
+    assert st["status"] == P.lra.LRA_ESINGULAR
+
+
+def test_argument_errors(P, h):
+    W = _dense(P, synth.config1(0))
+    bufs_I = torch.empty(8, dtype=torch.int64, device="cuda")
+    A = torch.empty((8, 256), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.LraError):   # k != l
+        P.lra_cross_approx(h, W, None, bufs_I, 8, 8, 9, 2, bufs_I, bufs_I, None, A, A)
+    with pytest.raises(P.LraError):   # r > k
+        P.lra_cross_approx(h, W, None, bufs_I, 9, 8, 8, 2, bufs_I, bufs_I, None, A, A)
+    M = P.lra.Multiplier(synth.multiplier_abridged(0, 256, 3, 8, "arht"))
+    M.mult = dict(M.mult, depth=9)   # 2^9 does not divide 256
+    Y = torch.empty((8, 256), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.LraError):
+        P.lra_preprocess(h, W, M, Y)
