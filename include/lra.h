@@ -167,6 +167,13 @@ lra_status lra_profile_enable(lra_handle h, int enable);
 int lra_profile_read(lra_handle h, int cap, const char **names /* host */, double *ms /* host */,
                      int64_t *counts /* host */);
 
+/* Diagnostics: clock64 cycle counters of the C-A kernel's phases, summed over problems
+   (CTA 0, thread 0): [0] block loads, [1] cold LUP, [2] warm-start gather, [3] Gauss-Jordan
+   inverse, [4] C = B X^{-1} product, [5] swap loops, [6] whole kernel, [7] pivot steps,
+   [8..14] sub-phases of a swap step and of the cluster exchange.
+   out16: host array of 16.  Synchronizes the device.  reset != 0 zeroes the counters. */
+lra_status lra_debug_counters(uint64_t *out16 /* host */, int reset);
+
 /* Thread-local message for the last non-OK status (never NULL). */
 const char *lra_last_error(void);
 

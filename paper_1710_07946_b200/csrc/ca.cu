@@ -1,17 +1,24 @@
 // ca.cu — stages 2-3 of Alg 10.2 with C-A iterations (Remark rerfnhmt),
-// each C-A step a maxvol on a tall-skinny block: Alg D.2 stage 1 (LUP cold start,
-// P:6550-6556) and the Alg D.1 swap loop with the rank-1 update.
+// each C-A step a maxvol on a tall-skinny N x q block: Alg D.2 stage 1 (LUP cold start,
+// P:6550-6556) or a warm start from the current slots, then the Alg D.1 swap loop
+// with the rank-1 update C <- C - C[:,j*](C[i*,:] - e_j*^T)/c_{i*j*}.
 //
-// One thread-block CLUSTER per problem.  The N x q C-matrix of the current step lives in
-// the cluster's distributed shared memory: CTA `rank` owns rows [rank*rpc, rank*rpc+rpc),
-// one row per thread, fp64 (complex128 for the ARFT sketch).  Every pivot decision is a
-// two-phase cluster reduction (global max, then the smallest row-major index with
-// |c| >= (1-tau) max, reading C11) through DSMEM exchange slots; the pivot row is fetched
-// from its owner's shared memory (ld.shared::cluster).  Rows in the selected set S are
-// kept implicit (they are identity rows of C = (I_q | C'), reading C12b), so no CTA ever
-// writes a row another CTA may be reading.  Blocks are gathered straight from W in HBM
-// (vertical W[:,J]: coalesced columns; horizontal W[I,:]^T: one sector per element).
-// The whole C-A (all sweeps, early exit) runs in one launch: no host round trips.
+// One thread-block CLUSTER per problem, ONE ROW OF THE BLOCK PER THREAD.  The row of the
+// C-matrix lives in that thread's registers (compile-time width Q >= q, zero padded), so
+// the LU and swap updates never touch shared memory.  Each pivot decision is
+//   CTA max  ->  CTA smallest index with |c| >= (1-tau) max  ->  ONE cluster exchange
+// of (max, index, value) triples through DSMEM, together with the CTA winner's row, which
+// the winning CTA publishes in its shared memory before the cluster barrier; every CTA
+// then copies the winning row (ld.shared::cluster).  The smallest-index rule (reading C11)
+// is exact: a CTA whose candidate value falls inside the tie window of the global max
+// (< 1e-12 relative) triggers a second, exact exchange (deterministic in every CTA).
+// C = B * X^{-1} is formed by an in-shared-memory Gauss-Jordan inverse of the q x q X
+// (X = B[S,:] for a warm start, X = L_S after the cold LUP, where the rows hold their LU
+// multipliers) followed by a register-accumulated product (fp64 FMA bound).  The selected
+// rows are implicit identity rows of C = (I_q | C') (reading C12b).  Blocks are gathered
+// straight from W (vertical W[:,J]: coalesced columns; horizontal W[I,:]^T: one sector
+// per element, 16 loads in flight per thread).  The whole C-A (all sweeps, early exit)
+// is one launch.  The complex (ARFT) stage-2 maxvol uses a shared-memory row variant.
 #include <cooperative_groups.h>
 #include <climits>
 
@@ -21,193 +28,711 @@ namespace cg = cooperative_groups;
 
 namespace lra {
 
+// Phase timers (clock64 cycles of CTA 0, thread 0 of every problem; read by
+// lra_debug_counters): 0 load, 1 cold LU, 2 warm gather, 3 Gauss-Jordan, 4 product,
+// 5 swap loop, 6 whole kernel, 7 pivot steps (count).
+__device__ unsigned long long g_ca_cyc[16];
+#define CA_MARK(k) do { if (threadIdx.x == 0 && c.rank == 0) { long long _n = clock64(); atomicAdd(&g_ca_cyc[k], (unsigned long long)(_n - _tm)); _tm = _n; } } while (0)
+#define CA_T0() long long _t0 = clock64()
+#define CA_T1(k) do { if (threadIdx.x == 0 && c.rank == 0) atomicAdd(&g_ca_cyc[k], (unsigned long long)(clock64() - _t0)); } while (0)
+
+struct Tri {
+  double M;
+  long long idx;
+  double v;
+};
 
 struct CAShared {
   long long Isl[LRA_QMAX], Jsl[LRA_QMAX];
+  unsigned long long rk[2][32];
+  unsigned ri[2][32];
+  double rv[2][32];
+  Tri xt[2];
+  Tri xin[2][16];              // triples pushed by every CTA of the cluster (slot = rank)
+  __align__(16) double pub[2][LRA_QMAX * 2];   // published candidate row (complex: 2x)
+  __align__(16) double prow[LRA_QMAX * 2];
+  __align__(16) double pm[LRA_QMAX];           // pivot row prepared for the update
+  double rc;                                   // 1 / pivot (swap steps)
+  double fcol[LRA_QMAX];
   double xd[2];
   long long xi[2];
-  double red_d[LRA_NT / 32];
-  long long red_i[LRA_NT / 32];
   double bd;
   long long bi;
   int piv[LRA_QMAX];
   int sing;
+  unsigned long long gk[2][32];   // Gauss-Jordan: per-warp pivot candidates
+  int gr[2][32];
+  __align__(16) double gp[2][128];   // Gauss-Jordan: scaled pivot row
+  double gd[2];
+  double dM;                   // exchange decision (written by warp 0)
+  long long dbest;
+  int damb;
 };
 
 struct Ctx {
   CAShared *sh;
-  unsigned char *smem_dyn;     // [Cs | Ls | prow | rmax | inS]
-  void *Cs;                    // rpc x qp of T
-  double *Ls;                  // L_S packed (cold) or G^T LU (warm, real)
-  void *prow;                  // q of T
-  double *rmax;                // rpc
-  unsigned char *inS;          // rpc
-  int rank, cs, rpc, qp, q, tid, lane, warp;
+  void *Cs;                    // rpc x qp (block rows; complex path: the C rows)
+  double *X;                   // q x QX (Gauss-Jordan), or packed L_S (complex path)
+  double *rmax;                // rpc   (complex path)
+  unsigned char *inS;          // rpc   (complex path)
+  int rank, cs, rpc, qp, q, QX, R0, AS, tid, lane, warp, nt, nw;
   int par;                     // exchange slot parity (identical in every CTA)
+  int ib;                      // column offset of the carried G^{-1} inside aug (0 or Q)
+  int rb;                      // CTA reduction buffer parity
   double tau, tol;
 };
 
-// ------------------------------------------------------------------ reductions
-__device__ double cta_max(Ctx &c, double v) {
-  v = warp_max(v);
-  if (c.lane == 0) c.sh->red_d[c.warp] = v;
-  __syncthreads();
-  if (c.warp == 0) {
-    double x = c.lane < LRA_NT / 32 ? c.sh->red_d[c.lane] : -INFINITY;
-    x = warp_max(x);
-    if (c.lane == 0) c.sh->bd = x;
-  }
-  __syncthreads();
-  return c.sh->bd;
-}
-__device__ long long cta_min(Ctx &c, long long v) {
-  v = warp_min_ll(v);
-  if (c.lane == 0) c.sh->red_i[c.warp] = v;
-  __syncthreads();
-  if (c.warp == 0) {
-    long long x = c.lane < LRA_NT / 32 ? c.sh->red_i[c.lane] : LLONG_MAX;
-    x = warp_min_ll(x);
-    if (c.lane == 0) c.sh->bi = x;
-  }
-  __syncthreads();
-  return c.sh->bi;
-}
-// Cluster-wide max: every CTA reduces the same CS partials in the same order, so all
-// CTAs take the same decision.  Slots alternate parity; a slot is rewritten only after
-// the next cluster barrier, by which time every reader of its previous value is done.
-__device__ double cluster_max(Ctx &c, double v) {
-  v = cta_max(c, v);
-  if (c.cs == 1) return v;
-  cg::cluster_group cl = cg::this_cluster();
-  const int p = c.par;
-  c.par ^= 1;
-  if (c.tid == 0) c.sh->xd[p] = v;
-  cl.sync();
-  if (c.warp == 0) {
-    double x = c.lane < c.cs ? *cl.map_shared_rank(&c.sh->xd[p], c.lane) : -INFINITY;
-    x = warp_max(x);
-    if (c.lane == 0) c.sh->bd = x;
-  }
-  __syncthreads();
-  return c.sh->bd;
-}
-__device__ long long cluster_min(Ctx &c, long long v) {
-  v = cta_min(c, v);
-  if (c.cs == 1) return v;
-  cg::cluster_group cl = cg::this_cluster();
-  const int p = c.par;
-  c.par ^= 1;
-  if (c.tid == 0) c.sh->xi[p] = v;
-  cl.sync();
-  if (c.warp == 0) {
-    long long x = c.lane < c.cs ? *cl.map_shared_rank(&c.sh->xi[p], c.lane) : LLONG_MAX;
-    x = warp_min_ll(x);
-    if (c.lane == 0) c.sh->bi = x;
-  }
-  __syncthreads();
-  return c.sh->bi;
-}
 __device__ __forceinline__ void cluster_barrier(const Ctx &c) {
   if (c.cs > 1) cg::this_cluster().sync();
   else __syncthreads();
 }
-// pointer to element (row, col) of the C-matrix held by CTA `owner`
 template <typename T>
-__device__ __forceinline__ const T *remote_row(const Ctx &c, int owner, int row_loc) {
-  T *base = reinterpret_cast<T *>(c.Cs) + (size_t)row_loc * c.qp;
-  if (c.cs == 1) return base;
-  return cg::this_cluster().map_shared_rank(base, owner);
+__device__ __forceinline__ T *remote(const Ctx &c, T *p, int rank) {
+  if (c.cs == 1) return p;
+  return cg::this_cluster().map_shared_rank(p, rank);
+}
+
+// ------------------------------------------------------ CTA reductions (1 barrier each)
+// Non-negative doubles order like their bit patterns, so maxima are taken on 64-bit keys
+// with two redux.sync.max.u32 (high word, then low word among the high-word winners);
+// negative sentinels map to key 0.  Index minima use redux.sync.min.u32 (indices < 2^31),
+// the value riding along from the winning lane by one shuffle.
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  return v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+}
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
+  const unsigned hi = (unsigned)(k >> 32);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned)k : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
+__device__ __forceinline__ void warp_min_idx(unsigned &i, double &v) {
+  const unsigned m = __reduce_min_sync(0xffffffffu, i);
+  const int src = __ffs(__ballot_sync(0xffffffffu, i == m)) - 1;
+  v = __shfl_sync(0xffffffffu, v, src);
+  i = m;
+}
+__device__ double cta_max1(Ctx &c, double v) {
+  unsigned long long k = warp_max_key(dkey(v));
+  const int b = c.rb;
+  c.rb ^= 1;
+  if (c.lane == 0) c.sh->rk[b][c.warp] = k;
+  __syncthreads();
+  k = warp_max_key(c.lane < c.nw ? c.sh->rk[b][c.lane] : 0ull);
+  return __longlong_as_double((long long)k);
+}
+__device__ void cta_minidx1(Ctx &c, unsigned &i, double &v) {
+  warp_min_idx(i, v);
+  const int b = c.rb;
+  c.rb ^= 1;
+  if (c.lane == 0) { c.sh->ri[b][c.warp] = i; c.sh->rv[b][c.warp] = v; }
+  __syncthreads();
+  i = c.lane < c.nw ? c.sh->ri[b][c.lane] : 0xffffffffu;
+  v = c.lane < c.nw ? c.sh->rv[b][c.lane] : 0.0;
+  warp_min_idx(i, v);
+}
+
+// Cluster exchange of the CTA triples (M_c, idx_c, v_c); the CTA winner's row has been
+// written to pub[p] by its owner thread.  Returns the global max M and the winning index
+// (smallest index with value >= (1-tau) M), `amb` if a tie-window candidate makes the CTA
+// candidates inexact; on success the winning row is copied into sh->prow (nwords doubles).
+struct Pick {
+  double M;
+  long long idx;
+  bool amb;
+};
+// mode 0: plain (prow only).  mode 1 (LU step t = arg): pm[j] = j > t ? prow[j] : 0.
+// mode 2 (swap): jstar = winner % q, pm = prow - e_jstar, rc = 1 / prow[jstar].
+__device__ Pick exchange(Ctx &c, int p, double Mc, long long idxc, double vc, int nwords, int mode = 0,
+                         int arg = 0) {
+  long long _tm = clock64();
+  // push this CTA's triple into slot `rank` of every CTA (remote stores; ordered by the
+  // cluster barrier's release/acquire), so the decision needs no remote load round trip
+  if (c.warp == 0 && c.lane < c.cs) *remote(c, &c.sh->xin[p][c.rank], c.lane) = Tri{Mc, idxc, vc};
+  cluster_barrier(c);
+  CA_MARK(11);
+  if (c.warp == 0) {
+    Tri t{-INFINITY, LLONG_MAX, 0.0};
+    if (c.lane < c.cs) t = c.sh->xin[p][c.lane];
+    const double M = __longlong_as_double((long long)warp_max_key(dkey(t.M)));
+    const double thr = (1.0 - c.tau) * M;
+    const long long cand = (t.M >= thr && t.v >= thr) ? t.idx : LLONG_MAX;
+    const int amb = __any_sync(0xffffffffu, c.lane < c.cs && t.M >= thr && t.v < thr);
+    const long long best = warp_min_ll(cand);
+    const int wr = __ffs(__ballot_sync(0xffffffffu, c.lane < c.cs && cand == best && best != LLONG_MAX)) - 1;
+    if (!amb && wr >= 0) {
+      const double *src = remote(c, &c.sh->pub[p][0], wr);
+      const int js = (mode == 2) ? (int)(best % c.q) : -1;
+      for (int j = c.lane; j < nwords; j += 32) {
+        const double x = src[j];
+        c.sh->prow[j] = x;
+        if (mode == 1) c.sh->pm[j] = (j > arg) ? x : 0.0;
+        if (mode == 2) {
+          c.sh->pm[j] = (j == js) ? x - 1.0 : x;
+          if (j == js) c.sh->rc = 1.0 / x;
+        }
+      }
+    }
+    if (c.lane == 0) {
+      c.sh->dM = M;
+      c.sh->dbest = best;
+      c.sh->damb = amb;
+    }
+  }
+  __syncthreads();
+  CA_MARK(12);
+  return Pick{c.sh->dM, c.sh->dbest, c.sh->damb != 0};
+}
+
+// ------------------------------------------------------------------ register rows
+// A block row is held by TPR consecutive lanes ("group"), lane s of the group owning the
+// W = Q/TPR contiguous columns [s*W, s*W + W).  Per-row quantities are combined with
+// xor-shuffles inside the group; selects / maxima use log-depth trees.
+template <int W>
+__device__ __forceinline__ double tsel(const double (&r)[W], int w) {   // r[w], runtime w
+  double v[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = r[i];
+#pragma unroll
+  for (int span = 1; span < W; span <<= 1) {
+#pragma unroll
+    for (int i = 0; i + span < W; i += 2 * span) v[i] = (w & span) ? v[i + span] : v[i];
+  }
+  return v[0];
+}
+template <int W>
+__device__ __forceinline__ double tmaxabs(const double (&r)[W]) {
+  double v[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = fabs(r[i]);
+#pragma unroll
+  for (int span = 1; span < W; span <<= 1) {
+#pragma unroll
+    for (int i = 0; i + span < W; i += 2 * span) v[i] = fmax(v[i], v[i + span]);
+  }
+  return v[0];
+}
+// smallest local column w with |r[w]| >= thr (and global column < q), else W; value in v
+template <int W>
+__device__ __forceinline__ int tfirst(const double (&r)[W], double thr, int jbase, int q, double &v) {
+  unsigned mask = 0;
+#pragma unroll
+  for (int i = 0; i < W; ++i) mask |= ((jbase + i < q) && fabs(r[i]) >= thr) ? (1u << i) : 0u;
+  if (!mask) return W;
+  const int w = __ffs(mask) - 1;
+  v = fabs(tsel<W>(r, w));
+  return w;
+}
+template <int TPR>
+__device__ __forceinline__ double gmax(double v) {
+#pragma unroll
+  for (int o = 1; o < TPR; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int TPR>
+__device__ __forceinline__ void gminpair(int &j, double &v) {
+#pragma unroll
+  for (int o = 1; o < TPR; o <<= 1) {
+    int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    if (oj < j) { j = oj; v = ov; }
+  }
+}
+template <int TPR>
+__device__ __forceinline__ double gbcast(double v, int lane, int s) {
+  return TPR == 1 ? v : __shfl_sync(0xffffffffu, v, (lane & ~(TPR - 1)) | s);
 }
 
 // ------------------------------------------------------------------ block loads
-template <typename T>
-__device__ void load_Y(Ctx &c, const void *Yb, int64_t ldy, int64_t N) {
-  const int64_t r0 = (int64_t)c.rank * c.rpc;
-  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
-  T *Cs = reinterpret_cast<T *>(c.Cs);
-  const T *Y = reinterpret_cast<const T *>(Yb);
-  for (int e = c.tid; e < nloc * c.q; e += LRA_NT) {
-    int j = e / nloc, i = e % nloc;
-    Cs[(size_t)i * c.qp + j] = Y[(int64_t)j * ldy + r0 + i];
-  }
-}
-// vertical block W[:, J] (N = m rows)
-__device__ void load_cols(Ctx &c, const OpView &op, const long long *J, int64_t N) {
-  const int64_t r0 = (int64_t)c.rank * c.rpc;
-  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
+// Row i of the CTA (global block row r0 + i) is loaded by its TPR lanes, 8 loads in flight.
+template <int TPR, typename F>
+__device__ __forceinline__ void load_rows(Ctx &c, int nloc, F &&at) {
   double *Cs = reinterpret_cast<double *>(c.Cs);
-  for (int e = c.tid; e < nloc * c.q; e += LRA_NT) {
-    int j = e / nloc, i = e % nloc;
-    Cs[(size_t)i * c.qp + j] = op.at(r0 + i, J[j]);
-  }
-}
-// horizontal block W[I, :]^T (N = n rows; block row = column of W)
-__device__ void load_rowsT(Ctx &c, const OpView &op, const long long *I, int64_t N) {
-  const int64_t r0 = (int64_t)c.rank * c.rpc;
-  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
-  double *Cs = reinterpret_cast<double *>(c.Cs);
-  for (int e = c.tid; e < nloc * c.q; e += LRA_NT) {
-    int s = e / nloc, i = e % nloc;
-    Cs[(size_t)i * c.qp + s] = op.at(I[s], r0 + i);
+  const int i = c.tid / TPR, s = c.tid % TPR;
+  if (i >= nloc) return;
+  for (int j0 = s; j0 < c.q; j0 += 8 * TPR) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u * TPR < c.q) v[u] = at(i, j0 + u * TPR);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u * TPR < c.q) Cs[(size_t)i * c.qp + j0 + u * TPR] = v[u];
   }
 }
 
-// ------------------------------------------------------------------ maxvol pieces
+// Operand access specialised at compile time (keeps the kernel's code small).
+template <int OPK>
+__device__ __forceinline__ double op_at(const OpView &op, int64_t i, int64_t j) {
+  if (OPK == 0) return (double)__ldg((const float *)op.w + j * op.ldw + i);
+  if (OPK == 1) return __ldg((const double *)op.w + j * op.ldw + i);
+  return op.f.at(i, j);
+}
+
+// ------------------------------------------------------------------ Gauss-Jordan inverse
+// The q x q matrix X sits in the left part of the augmented [X | I] (row stride AS, right
+// part at column R0 = Q, zero padded to width Q).  Gauss-Jordan with partial pivoting
+// WITHOUT physical row swaps: step t picks the row p_t (not yet a pivot) of max |X[a][t]|
+// (first on ties), scales it and eliminates column t from every other row.  The matrix
+// is held in registers (warp w: rows w + 16k; lane l: columns l + 32m), so a step costs
+// two barriers and ~100 bytes of shared traffic: per-warp pivot candidates, then the
+// scaled pivot row.  Afterwards row t of X^{-1} is the right part of row piv[t], which is
+// copied to the left part (rows t).  Every CTA computes the same result.  False if singular.
+__device__ __noinline__ bool gj_inverse(CAShared *sh, double *A, int q, int R0, int AS, int nt) {
+  const int WD = 2 * R0;                     // [X | I] width (row stride AS >= WD)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double x[4][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int a = warp + k * nw, bc = lane + 32 * m;
+      x[k][m] = (a < q && bc < WD) ? A[a * AS + bc] : 0.0;
+    }
+  unsigned usedk = 0;                        // my rows already used as pivots (bit k)
+  for (int t = 0; t < q; ++t) {
+    const int mt = t >> 5, lt = t & 31, sl = t & 1;
+    double v[4];
+    unsigned long long key = 0ull;
+    int arow = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double xv = x[k][0];
+#pragma unroll
+      for (int m = 1; m < 4; ++m) xv = (mt == m) ? x[k][m] : xv;
+      v[k] = __shfl_sync(0xffffffffu, xv, lt);
+      const int a = warp + k * nw;
+      if (a < q && !((usedk >> k) & 1u)) {
+        const double av = fabs(v[k]);
+        const unsigned long long kk = (av != av) ? 0x7ff8000000000000ull : dkey(av);
+        if (arow == 0x7fffffff || kk > key) { key = kk; arow = a; }
+      }
+    }
+    if (lane == 0) { sh->gk[sl][warp] = key; sh->gr[sl][warp] = arow; }
+    __syncthreads();
+    unsigned long long ck = lane < nw ? sh->gk[sl][lane] : 0ull;
+    const int cr = lane < nw ? sh->gr[sl][lane] : 0x7fffffff;
+    const unsigned long long mk = warp_max_key(ck);
+    const int p = (int)__reduce_min_sync(0xffffffffu, (ck == mk && cr != 0x7fffffff) ? (unsigned)cr : 0xffffffffu);
+    if (p >= q) return false;
+    const int kp = p / nw;
+    if (tid == 0) sh->piv[t] = p;
+    if (warp == p % nw) {                    // owner of the pivot row publishes it scaled
+      const double d = v[kp == 0 ? 0 : (kp == 1 ? 1 : (kp == 2 ? 2 : 3))];
+      const double rd = 1.0 / d;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int bc = lane + 32 * m;
+        double xv = x[0][m];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) xv = (kp == k) ? x[k][m] : xv;
+        sh->gp[sl][bc] = (bc == t) ? 1.0 : xv * rd;
+      }
+      if (lane == 0) sh->gd[sl] = d;
+    }
+    __syncthreads();
+    const double d = sh->gd[sl];
+    if (!(fabs(d) > 0.0) || !isfinite(d)) return false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int a = warp + k * nw;
+      const bool isp = (a == p);
+      if (isp) usedk |= 1u << k;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int bc = lane + 32 * m;
+        const double pv = sh->gp[sl][bc];
+        x[k][m] = isp ? pv : ((bc == t) ? 0.0 : fma(-v[k], pv, x[k][m]));
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int a = warp + k * nw, bc = lane + 32 * m;
+      if (a < q && bc < WD) A[a * AS + bc] = x[k][m];
+    }
+  __syncthreads();
+  return true;
+}
+
+// out = base + sg * L * R on q x q blocks of aug (parts are column offsets, stride AS):
+// base = I (bp < 0) or part bp.  Warp w: rows w + 16k; lanes: columns lane, lane + 32.
+__device__ __forceinline__ void mm_small(const Ctx &c, int out, int lp, int rp, int bp, double sg) {
+  const int q = c.q, AS = c.AS;
+  double acc[4][2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = 0.0;
+  for (int t = 0; t < q; ++t) {
+    const double r0v = (c.lane < q) ? c.X[t * AS + rp + c.lane] : 0.0;
+    const double r1v = (c.lane + 32 < q) ? c.X[t * AS + rp + c.lane + 32] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = c.warp + k * c.nw;
+      const double l = (i < q) ? c.X[i * AS + lp + t] : 0.0;
+      acc[k][0] = fma(l, r0v, acc[k][0]);
+      acc[k][1] = fma(l, r1v, acc[k][1]);
+    }
+  }
+  __syncthreads();                           // out may alias an input part
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = c.warp + k * c.nw;
+    if (i >= q) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = c.lane + 32 * h;
+      if (j >= c.QX) continue;
+      double v = 0.0;
+      if (j < q) {
+        const double b = bp < 0 ? (i == j ? 1.0 : 0.0) : c.X[i * AS + bp + j];
+        v = fma(sg, acc[k][h], b);
+      }
+      c.X[i * AS + out + j] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// own W columns of (row input in Cs) * G^{-1};  G^{-1} = aug[t][ib .. ib+Q)
+template <int W>
+__device__ __forceinline__ void product(const Ctx &c, int i, int jb, int ib, double (&row)[W]) {
+  const double *Cs = reinterpret_cast<const double *>(c.Cs) + (size_t)i * c.qp;
+#pragma unroll
+  for (int w = 0; w < W; ++w) row[w] = 0.0;
+  for (int t = 0; t < c.q; ++t) {
+    const double b = Cs[t];
+    const double2 *xr = reinterpret_cast<const double2 *>(c.X + t * c.AS + ib + jb);
+#pragma unroll
+    for (int w = 0; w < W / 2; ++w) {
+      const double2 x = xr[w];
+      row[2 * w] = fma(b, x.x, row[2 * w]);
+      row[2 * w + 1] = fma(b, x.y, row[2 * w + 1]);
+    }
+  }
+}
+
 struct MVOut {
   int swaps, lu_steps;
   bool cap_hit;
   double cert;
 };
 
-// Alg D.2 stage 1: LU with partial pivoting (slack rule), pivots -> S; then C = L L_S^{-1}
-// for the non-pivot rows (C = B B_S^{-1}, Alg D.2 stage 2).  Returns false if singular.
-template <typename T>
-__device__ bool lup_cold(Ctx &c, int64_t N, long long *S) {
-  using K = Sc<T>;
-  T *Cs = reinterpret_cast<T *>(c.Cs);
-  T *prow = reinterpret_cast<T *>(c.prow);
-  T *Ls = reinterpret_cast<T *>(c.Ls);
+// ------------------------------------------------------------------ real maxvol (registers)
+// Block rows are in Cs (unchanged).  S: slot array (smem; cold: output, warm: input/output).
+// G^{-1} (G = B[S,:]) lives in aug (q rows of width 2Q, at column offset c.ib): a cold step
+// forms it by Gauss-Jordan on the gathered B[S,:]; every swap updates it with the same
+// rank-1 formula as C (it is C for the "rows" of I_q), and since each C-A step's
+// generator is the transpose of the previous step's final generator (W[I,J] vs W[I,J]^T),
+// a warm start only transposes the carried inverse.
+template <int Q, int TPR>
+__device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, bool cold, bool carried, int cap,
+                                            MVOut &o) {
+  constexpr int W = Q / TPR;
   const int64_t r0 = (int64_t)c.rank * c.rpc;
   const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
   const int q = c.q;
-  for (int i = c.tid; i < c.rpc; i += LRA_NT) c.inS[i] = 0;
+  const int ri = c.tid / TPR, sub = c.tid % TPR, jb = sub * W;
+  const bool has = ri < nloc;
+  const long long grow = r0 + ri;
+  const double *Cs = reinterpret_cast<const double *>(c.Cs) + (size_t)ri * c.qp;
+  double row[W];
+  int myslot = -1;
+  o = MVOut{0, 0, false, 0.0};
+  CA_T0();
+  if (cold) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) row[w] = (has && jb + w < q) ? Cs[jb + w] : 0.0;
+    // ---- Alg D.2 stage 1: LUP with the slack pivot rule; bit-identical to the oracle
+    for (int t = 0; t < q; ++t) {
+      const int st = t / W, wt = t - st * W;
+      const double x = gbcast<TPR>(tsel<W>(row, wt), c.lane, st);   // B'[row, t]
+      double val = -1.0;
+      if (has && myslot < 0) val = (x != x) ? INFINITY : fabs(x);
+      const double Mc = cta_max1(c, val);
+      const double thrc = (1.0 - c.tau) * Mc;
+      unsigned ui = (has && myslot < 0 && val >= thrc) ? (unsigned)grow : 0xffffffffu;
+      double v = val;
+      cta_minidx1(c, ui, v);
+      const long long idx = ui == 0xffffffffu ? LLONG_MAX : (long long)ui;
+      int p = c.par;
+      c.par ^= 1;
+      if (has && grow == idx) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+      }
+      Pick pk = exchange(c, p, Mc, idx, v, Q, 1, t);
+      if (!(pk.M > 0.0) || !isfinite(pk.M)) return false;
+      if (pk.amb) {                                  // exact second round (tie window)
+        const double thr = (1.0 - c.tau) * pk.M;
+        unsigned u2 = (has && myslot < 0 && val >= thr) ? (unsigned)grow : 0xffffffffu;
+        double v2 = val;
+        cta_minidx1(c, u2, v2);
+        const long long i2 = u2 == 0xffffffffu ? LLONG_MAX : (long long)u2;
+        p = c.par;
+        c.par ^= 1;
+        if (has && grow == i2) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+        }
+        pk = exchange(c, p, pk.M, i2, v2, Q, 1, t);
+      }
+      const long long piv = pk.idx;
+      if (c.tid == 0) S[t] = piv;
+      if (has && grow == piv) myslot = t;
+      if (has && myslot < 0) {            // B'[i, j] -= (B'[i,t]/B'[p,t]) B'[p,j], j > t
+        const double f = x / c.sh->prow[t];
+        const double2 *pm2 = reinterpret_cast<const double2 *>(c.sh->pm + jb);
+#pragma unroll
+        for (int w = 0; w < W / 2; ++w) {   // pm = 0 for j <= t: those entries are unchanged
+          const double2 pv = pm2[w];
+          row[2 * w] = rsub_mul(row[2 * w], f, pv.x);
+          row[2 * w + 1] = rsub_mul(row[2 * w + 1], f, pv.y);
+        }
+      }
+    }
+    o.lu_steps = q;
+    __syncthreads();
+    CA_T1(1);
+  } else if (has) {
+    for (int s2 = 0; s2 < q; ++s2)
+      if (S[s2] == grow) myslot = s2;
+  }
+  {
+    CA_T0();
+    if (cold || !carried) {
+      // ---- G = B[S,:] gathered from the owners' shared memory, G^{-1} by Gauss-Jordan
+      cluster_barrier(c);                            // every CTA's block rows are loaded
+      for (int a = c.warp; a < q; a += c.nw) {       // [G | I]
+        const long long sr = S[a];
+        const double *src = remote(c, reinterpret_cast<const double *>(c.Cs), (int)(sr / c.rpc)) +
+                            (size_t)(sr % c.rpc) * c.qp;
+        for (int e = c.lane; e < 2 * Q; e += 32) {
+          double xv;
+          if (e < Q) xv = (e < q) ? src[e] : 0.0;
+          else xv = (e - Q == a) ? 1.0 : 0.0;
+          c.X[a * c.AS + e] = xv;
+        }
+      }
+      __syncthreads();
+      CA_T1(2);
+      CA_T0();
+      if (!gj_inverse(c.sh, c.X, q, Q, c.AS, c.nt)) return false;
+      // rows of G^{-1}: row t is the right part of row piv[t] -> left part, row t
+      for (int a = c.warp; a < q; a += c.nw) {
+        const int pr = c.sh->piv[a];
+        for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + e] = c.X[pr * c.AS + Q + e];
+      }
+      c.ib = 0;
+      __syncthreads();
+      CA_T1(3);
+    } else {
+      // ---- carried inverse X0 = (G_prev^{-1})^T = G^{-1} up to the rounding accumulated by
+      // the previous step's rank-1 updates; one Newton step X1 = X0 + X0 (I - G X0) against
+      // the freshly gathered G restores a fresh-solve accuracy.
+      const int cur = c.ib, pa = (cur + Q) % (3 * Q), pb = (cur + 2 * Q) % (3 * Q);
+      for (int a = c.warp; a < q; a += c.nw)         // X0 = cur^T -> part pa
+        for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + pa + e] = (e < q) ? c.X[e * c.AS + cur + a] : 0.0;
+      cluster_barrier(c);                            // every CTA's block rows are loaded
+      for (int a = c.warp; a < q; a += c.nw) {       // G = B[S,:] -> part pb
+        const long long sr = S[a];
+        const double *src = remote(c, reinterpret_cast<const double *>(c.Cs), (int)(sr / c.rpc)) +
+                            (size_t)(sr % c.rpc) * c.qp;
+        for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + pb + e] = (e < q) ? src[e] : 0.0;
+      }
+      __syncthreads();
+      mm_small(c, cur, pb, pa, -1, -1.0);            // R  = I - G X0   -> part cur
+      mm_small(c, pb, pa, cur, pa, 1.0);             // X1 = X0 + X0 R  -> part pb
+      c.ib = pb;
+      CA_T1(2);
+    }
+  }
+  {
+    CA_T0();
+    if (has && myslot < 0) product<W>(c, ri, jb, c.ib, row);
+    __syncthreads();
+    CA_T1(4);
+  }
+  double rmx = gmax<TPR>(tmaxabs<W>(row));
+  if (!(has && myslot < 0)) rmx = -1.0;
+  long long _ts = clock64();
+  // ---- Alg D.1 swap loop
+  for (int round = 0;; ++round) {
+    long long _tm = clock64();
+    const double Mc = cta_max1(c, rmx);
+    CA_MARK(8);
+    const double thrc = (1.0 - c.tau) * Mc;
+    int jl = Q;
+    double v = 0.0;
+    if (has && myslot < 0 && rmx >= thrc) {
+      const int w = tfirst<W>(row, thrc, jb, q, v);
+      jl = (w < W) ? jb + w : Q;
+    }
+    gminpair<TPR>(jl, v);
+    unsigned ui = (jl < q) ? (unsigned)(grow * q + jl) : 0xffffffffu;
+    cta_minidx1(c, ui, v);
+    const long long idx = ui == 0xffffffffu ? LLONG_MAX : (long long)ui;
+    CA_MARK(9);
+    int p = c.par;
+    c.par ^= 1;
+    if (has && idx != LLONG_MAX && grow == idx / q) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+    }
+    CA_MARK(10);
+    Pick pk = exchange(c, p, Mc, idx, v, Q, 2);
+    _tm = clock64();
+    if (!(pk.M == pk.M)) return false;
+    if (pk.M <= 1.0 + c.tol || o.swaps >= cap) {
+      o.cert = fmax(pk.M, 0.0);
+      o.cap_hit = pk.M > 1.0 + c.tol;
+      if (threadIdx.x == 0 && c.rank == 0) {
+        atomicAdd(&g_ca_cyc[5], (unsigned long long)(clock64() - _ts));
+        atomicAdd(&g_ca_cyc[7], (unsigned long long)(o.swaps + o.lu_steps));
+      }
+      return true;
+    }
+    if (pk.amb) {
+      const double thr = (1.0 - c.tau) * pk.M;
+      int j2 = Q;
+      double v2 = 0.0;
+      if (has && myslot < 0 && rmx >= thr) {
+        const int w = tfirst<W>(row, thr, jb, q, v2);
+        j2 = (w < W) ? jb + w : Q;
+      }
+      gminpair<TPR>(j2, v2);
+      unsigned u2 = (j2 < q) ? (unsigned)(grow * q + j2) : 0xffffffffu;
+      cta_minidx1(c, u2, v2);
+      const long long i2 = u2 == 0xffffffffu ? LLONG_MAX : (long long)u2;
+      p = c.par;
+      c.par ^= 1;
+      if (has && i2 != LLONG_MAX && grow == i2 / q) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+      }
+      pk = exchange(c, p, pk.M, i2, v2, Q, 2);
+    }
+    const long long istar = pk.idx / q;
+    const int jstar = (int)(pk.idx % q);
+    const int sj = jstar / W, wj = jstar - sj * W;
+    if (c.tid == 0) S[jstar] = istar;
+    if (has && myslot == jstar) {                    // leaves S: explicit row e_{j*}
+      myslot = -1;
+#pragma unroll
+      for (int w = 0; w < W; ++w) row[w] = (jb + w == jstar) ? 1.0 : 0.0;
+    }
+    if (has && grow == istar) myslot = jstar;        // enters S
+    const double xj = gbcast<TPR>(tsel<W>(row, wj), c.lane, sj);
+    const double rc = c.sh->rc;
+    if (has && myslot < 0) {           // C <- C - C[:,j*] (C[i*,:] - e_j*) / c
+      const double g = xj * rc;
+      const double2 *pm2 = reinterpret_cast<const double2 *>(c.sh->pm + jb);
+#pragma unroll
+      for (int w = 0; w < W / 2; ++w) {
+        const double2 pv = pm2[w];
+        row[2 * w] = fma(-g, pv.x, row[2 * w]);
+        row[2 * w + 1] = fma(-g, pv.y, row[2 * w + 1]);
+      }
+    }
+    // the same update of the carried G^{-1} (every CTA keeps an identical copy)
+    for (int a = c.warp; a < q; a += c.nw) {
+      double *ir = c.X + a * c.AS + c.ib;
+      const double g = ir[jstar] * rc;
+      __syncwarp();
+      for (int e = c.lane; e < q; e += 32) ir[e] = fma(-g, c.sh->pm[e], ir[e]);
+    }
+    rmx = gmax<TPR>(tmaxabs<W>(row));
+    if (!(has && myslot < 0)) rmx = -1.0;
+    ++o.swaps;
+    CA_MARK(14);
+  }
+}
+
+// ------------------------------------------------- complex maxvol (ARFT sketch, smem rows)
+__device__ double cta_max_c(Ctx &c, double v) { return cta_max1(c, v); }
+__device__ long long cta_min_c(Ctx &c, long long v) {
+  double dummy = 0.0;
+  unsigned u = v == LLONG_MAX ? 0xffffffffu : (unsigned)v;
+  cta_minidx1(c, u, dummy);
+  return u == 0xffffffffu ? LLONG_MAX : (long long)u;
+}
+__device__ double cluster_max_c(Ctx &c, double v) {
+  v = cta_max_c(c, v);
+  if (c.cs == 1) return v;
+  cg::cluster_group cl = cg::this_cluster();
+  const int p = c.par;
+  c.par ^= 1;
+  if (c.tid == 0) c.sh->xd[p] = v;
+  cl.sync();
+  double x = c.lane < c.cs ? *cl.map_shared_rank(&c.sh->xd[p], c.lane) : -INFINITY;
+  return warp_max(x);
+}
+__device__ long long cluster_min_c(Ctx &c, long long v) {
+  v = cta_min_c(c, v);
+  if (c.cs == 1) return v;
+  cg::cluster_group cl = cg::this_cluster();
+  const int p = c.par;
+  c.par ^= 1;
+  if (c.tid == 0) c.sh->xi[p] = v;
+  cl.sync();
+  long long x = c.lane < c.cs ? *cl.map_shared_rank(&c.sh->xi[p], c.lane) : LLONG_MAX;
+  return warp_min_ll(x);
+}
+__device__ const cplx *remote_row_c(const Ctx &c, int owner, int row_loc) {
+  cplx *base = reinterpret_cast<cplx *>(c.Cs) + (size_t)row_loc * c.qp;
+  return remote(c, base, owner);
+}
+
+__device__ __noinline__ bool maxvol_complex(Ctx &c, int64_t N, long long *S, int cap, MVOut &o) {
+  using K = Sc<cplx>;
+  cplx *Cs = reinterpret_cast<cplx *>(c.Cs);
+  cplx *prow = reinterpret_cast<cplx *>(c.sh->prow);
+  cplx *Ls = reinterpret_cast<cplx *>(c.X);
+  const int64_t r0 = (int64_t)c.rank * c.rpc;
+  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
+  const int q = c.q;
+  o = MVOut{0, q, false, 0.0};
+  for (int i = c.tid; i < c.rpc; i += c.nt) c.inS[i] = 0;
   __syncthreads();
   for (int t = 0; t < q; ++t) {
     double lm = -1.0;
-    for (int i = c.tid; i < nloc; i += LRA_NT)
-      if (!c.inS[i]) lm = fmax(lm, K::abs(Cs[(size_t)i * c.qp + t]));
-    const double M = cluster_max(c, lm);
+    for (int i = c.tid; i < nloc; i += c.nt)
+      if (!c.inS[i]) {
+        double a = K::abs(Cs[(size_t)i * c.qp + t]);
+        lm = fmax(lm, a != a ? INFINITY : a);
+      }
+    const double M = cluster_max_c(c, lm);
     if (!(M > 0.0) || !isfinite(M)) return false;
     const double thr = (1.0 - c.tau) * M;
     long long li = LLONG_MAX;
-    for (int i = c.tid; i < nloc; i += LRA_NT)
+    for (int i = c.tid; i < nloc; i += c.nt)
       if (!c.inS[i] && K::abs(Cs[(size_t)i * c.qp + t]) >= thr) { li = r0 + i; break; }
-    const long long p = cluster_min(c, li);
+    const long long p = cluster_min_c(c, li);
     const int owner = (int)(p / c.rpc), ploc = (int)(p % c.rpc);
-    if (c.tid < q) prow[c.tid] = remote_row<T>(c, owner, ploc)[c.tid];
+    if (c.tid < q) prow[c.tid] = remote_row_c(c, owner, ploc)[c.tid];
     if (c.tid == 0) {
       S[t] = p;
       if (owner == c.rank) c.inS[ploc] = 1;
     }
     __syncthreads();
-    if (c.tid < t) Ls[t * (t - 1) / 2 + c.tid] = prow[c.tid];   // L_S[t, 0..t-1]
-    const T piv = prow[t];
-    for (int i = c.tid; i < nloc; i += LRA_NT) {
+    if (c.tid < t) Ls[t * (t - 1) / 2 + c.tid] = prow[c.tid];
+    const cplx piv = prow[t];
+    for (int i = c.tid; i < nloc; i += c.nt) {
       if (c.inS[i]) continue;
-      T *row = Cs + (size_t)i * c.qp;
-      const T f = K::div(row[t], piv);
-      row[t] = f;                                               // multiplier L[i, t]
+      cplx *row = Cs + (size_t)i * c.qp;
+      const cplx f = K::div(row[t], piv);
+      row[t] = f;
       for (int j = t + 1; j < q; ++j) row[j] = K::sub_mul(row[j], f, prow[j]);
     }
     __syncthreads();
   }
-  // C_i = l_i L_S^{-1}:  c_j = l_j - sum_{t>j} c_t L_S[t, j],  j = q-1 .. 0
-  for (int i = c.tid; i < nloc; i += LRA_NT) {
+  for (int i = c.tid; i < nloc; i += c.nt) {
     if (c.inS[i]) continue;
-    T *row = Cs + (size_t)i * c.qp;
+    cplx *row = Cs + (size_t)i * c.qp;
     double mx = 0.0;
     for (int j = q - 1; j >= 0; --j) {
-      T acc = row[j];
+      cplx acc = row[j];
       for (int t = j + 1; t < q; ++t) acc = K::fsub_mul(acc, row[t], Ls[t * (t - 1) / 2 + j]);
       row[j] = acc;
       mx = fmax(mx, K::abs(acc));
@@ -215,149 +740,51 @@ __device__ bool lup_cold(Ctx &c, int64_t N, long long *S) {
     c.rmax[i] = mx;
   }
   __syncthreads();
-  return true;
-}
-
-// Warm start (real): C = B * G^{-1}, G = B[S,:], by LU of G^T with partial pivoting in
-// every CTA (redundantly, identical results) and one forward/back substitution per row.
-__device__ bool warm_start(Ctx &c, int64_t N, const long long *S) {
-  double *Cs = reinterpret_cast<double *>(c.Cs);
-  double *G = c.Ls;                 // q x q, G[a*q + b] = G^T[a][b] = B[S[b]][a]
-  const int64_t r0 = (int64_t)c.rank * c.rpc;
-  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
-  const int q = c.q;
-  for (int i = c.tid; i < c.rpc; i += LRA_NT) c.inS[i] = 0;
-  __syncthreads();
-  if (c.tid < q) {
-    long long s = S[c.tid];
-    if (s / c.rpc == c.rank) c.inS[s % c.rpc] = 1;
-  }
-  cluster_barrier(c);               // every CTA's block rows are loaded
-  for (int e = c.tid; e < q * q; e += LRA_NT) {
-    int a = e / q, b = e % q;
-    long long s = S[b];
-    G[a * q + b] = remote_row<double>(c, (int)(s / c.rpc), (int)(s % c.rpc))[a];
-  }
-  __syncthreads();
-  // LU of G^T (in G) with partial pivoting (first max on ties)
-  for (int t = 0; t < q; ++t) {
-    if (c.warp == 0) {
-      double best = -1.0;
-      int bi = t;
-      for (int a = t + c.lane; a < q; a += 32) {
-        double v = fabs(G[a * q + t]);
-        if (v > best) { best = v; bi = a; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (c.lane == 0) {
-        c.sh->piv[t] = bi;
-        c.sh->sing = !(best > 0.0) || !isfinite(best);
-      }
-      __syncwarp();
-      if (bi != t)
-        for (int b = c.lane; b < q; b += 32) {
-          double x = G[t * q + b];
-          G[t * q + b] = G[bi * q + b];
-          G[bi * q + b] = x;
-        }
-    }
-    __syncthreads();
-    if (c.sh->sing) return false;
-    const double d = G[t * q + t];
-    for (int a = t + 1 + c.tid; a < q; a += LRA_NT) G[a * q + t] /= d;
-    __syncthreads();
-    const int w = q - t - 1;
-    for (int e = c.tid; e < w * w; e += LRA_NT) {
-      int a = t + 1 + e / w, b = t + 1 + e % w;
-      G[a * q + b] = fma(-G[a * q + t], G[t * q + b], G[a * q + b]);
-    }
-    __syncthreads();
-  }
-  // rows: solve G^T x = b  (x = C row)
-  for (int i = c.tid; i < nloc; i += LRA_NT) {
-    if (c.inS[i]) continue;
-    double *row = Cs + (size_t)i * c.qp;
-    for (int t = 0; t < q; ++t) {
-      int p = c.sh->piv[t];
-      if (p != t) { double x = row[t]; row[t] = row[p]; row[p] = x; }
-    }
-    for (int a = 1; a < q; ++a) {
-      double acc = row[a];
-      for (int t = 0; t < a; ++t) acc = fma(-G[a * q + t], row[t], acc);
-      row[a] = acc;
-    }
-    double mx = 0.0;
-    for (int a = q - 1; a >= 0; --a) {
-      double acc = row[a];
-      for (int t = a + 1; t < q; ++t) acc = fma(-G[a * q + t], row[t], acc);
-      acc /= G[a * q + a];
-      row[a] = acc;
-      mx = fmax(mx, fabs(acc));
-    }
-    c.rmax[i] = mx;
-  }
-  __syncthreads();
-  return true;
-}
-
-// Alg D.1 swap loop with the rank-1 update C <- C - C[:,j*] (C[i*,:] - e_j*^T) / c_{i*j*}.
-template <typename T>
-__device__ MVOut swap_loop(Ctx &c, int64_t N, long long *S, int cap) {
-  using K = Sc<T>;
-  T *Cs = reinterpret_cast<T *>(c.Cs);
-  T *prow = reinterpret_cast<T *>(c.prow);
-  const int64_t r0 = (int64_t)c.rank * c.rpc;
-  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
-  const int q = c.q;
-  MVOut o{0, 0, false, 0.0};
   for (;;) {
     double lm = 0.0;
-    for (int i = c.tid; i < nloc; i += LRA_NT)
+    for (int i = c.tid; i < nloc; i += c.nt)
       if (!c.inS[i]) lm = fmax(lm, c.rmax[i]);
-    const double M = cluster_max(c, lm);
+    const double M = cluster_max_c(c, lm);
+    if (!(M == M)) return false;
     if (M <= 1.0 + c.tol || o.swaps >= cap) {
       o.cert = M;
       o.cap_hit = M > 1.0 + c.tol;
-      return o;
+      return true;
     }
     const double thr = (1.0 - c.tau) * M;
     long long li = LLONG_MAX;
-    for (int i = c.tid; i < nloc && li == LLONG_MAX; i += LRA_NT) {
+    for (int i = c.tid; i < nloc && li == LLONG_MAX; i += c.nt) {
       if (c.inS[i] || c.rmax[i] < thr) continue;
-      const T *row = Cs + (size_t)i * c.qp;
+      const cplx *row = Cs + (size_t)i * c.qp;
       for (int j = 0; j < q; ++j)
         if (K::abs(row[j]) >= thr) { li = (r0 + i) * (long long)q + j; break; }
     }
-    const long long L = cluster_min(c, li);
+    const long long L = cluster_min_c(c, li);
     const long long istar = L / q;
     const int jstar = (int)(L % q);
     const int owner = (int)(istar / c.rpc);
-    if (c.tid < q) prow[c.tid] = remote_row<T>(c, owner, (int)(istar % c.rpc))[c.tid];
+    if (c.tid < q) prow[c.tid] = remote_row_c(c, owner, (int)(istar % c.rpc))[c.tid];
     const long long sold = S[jstar];
-    __syncthreads();                 // S[jstar] read by all before it changes
+    __syncthreads();
     if (c.tid == 0) {
       S[jstar] = istar;
       if (owner == c.rank) c.inS[istar % c.rpc] = 1;
-      if (sold / c.rpc == c.rank) {  // the leaving row becomes an explicit row e_{j*}
+      if (sold / c.rpc == c.rank) {
         int sl = (int)(sold % c.rpc);
         c.inS[sl] = 0;
-        T *row = Cs + (size_t)sl * c.qp;
+        cplx *row = Cs + (size_t)sl * c.qp;
         for (int j = 0; j < q; ++j) row[j] = (j == jstar) ? K::one() : K::zero();
       }
     }
     __syncthreads();
-    const T piv = prow[jstar];
-    for (int i = c.tid; i < nloc; i += LRA_NT) {
+    const cplx piv = prow[jstar];
+    for (int i = c.tid; i < nloc; i += c.nt) {
       if (c.inS[i]) continue;
-      T *row = Cs + (size_t)i * c.qp;
-      const T g = K::div(row[jstar], piv);
+      cplx *row = Cs + (size_t)i * c.qp;
+      const cplx g = K::div(row[jstar], piv);
       double mx = 0.0;
       for (int j = 0; j < q; ++j) {
-        T v = (j == jstar) ? g : K::fsub_mul(row[j], g, prow[j]);
+        cplx v = (j == jstar) ? g : K::fsub_mul(row[j], g, prow[j]);
         row[j] = v;
         mx = fmax(mx, K::abs(v));
       }
@@ -368,101 +795,142 @@ __device__ MVOut swap_loop(Ctx &c, int64_t N, long long *S, int cap) {
   }
 }
 
-template <typename T>
-__device__ bool maxvol_cold(Ctx &c, int64_t N, long long *S, int cap, MVOut &o) {
-  if (!lup_cold<T>(c, N, S)) return false;
-  o = swap_loop<T>(c, N, S, cap);
-  o.lu_steps = c.q;
-  return true;
-}
-__device__ bool maxvol_warm(Ctx &c, int64_t N, long long *S, int cap, MVOut &o) {
-  if (!warm_start(c, N, S)) return false;
-  o = swap_loop<double>(c, N, S, cap);
-  o.lu_steps = 0;
-  return true;
-}
-
-// ------------------------------------------------------------------ the C-A kernel
-__global__ void __launch_bounds__(LRA_NT, 1) k_ca(CAArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ CAShared sh;
-  Ctx c;
-  c.sh = &sh;
+// ------------------------------------------------------------------ context setup
+template <int Q, int NT>
+__device__ __forceinline__ void ctx_init(Ctx &c, CAShared *sh, unsigned char *dsm, const CAArgs &a) {
+  c.sh = sh;
   c.cs = a.cs;
   c.rank = (a.cs > 1) ? (int)cg::this_cluster().block_rank() : 0;
   c.rpc = a.rpc;
   c.qp = a.qp;
   c.q = a.q;
+  c.QX = Q;
+  c.R0 = Q;
+  c.AS = 3 * Q;
+  c.ib = 0;
   c.tid = threadIdx.x;
   c.lane = threadIdx.x & 31;
   c.warp = threadIdx.x >> 5;
+  c.nt = NT;
+  c.nw = NT / 32;
   c.par = 0;
+  c.rb = 0;
   c.tau = a.tau;
   c.tol = a.tol;
   const size_t esz = a.y_complex ? 16 : 8;
   size_t off = 0;
-  c.Cs = dsm + off;
+  c.Cs = dsm;
   off += (size_t)a.rpc * a.qp * esz;
   off = (off + 15) & ~(size_t)15;
-  c.Ls = reinterpret_cast<double *>(dsm + off);
-  size_t lsz = (size_t)a.q * a.q * 8;
-  size_t lsz2 = (size_t)a.q * (a.q - 1) / 2 * esz;
-  off += lsz > lsz2 ? lsz : lsz2;
-  off = (off + 15) & ~(size_t)15;
-  c.prow = dsm + off;
-  off += (size_t)a.q * 16;
+  c.X = reinterpret_cast<double *>(dsm + off);
+  off += a.y_complex ? (size_t)a.q * (a.q - 1) / 2 * 16 : (size_t)a.q * 3 * Q * 8;
   c.rmax = reinterpret_cast<double *>(dsm + off);
   off += (size_t)a.rpc * 8;
   c.inS = dsm + off;
+}
 
+// Stage 2 on a complex (ARFT) sketch: I0 <- maxvol(Y), written to a.I; its counters go
+// to a.yinfo[4b..4b+3] = (status, swaps, cap_hit, lu_steps) for the C-A kernel.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_ca_ycplx(CAArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ CAShared sh;
+  Ctx c;
+  ctx_init<LRA_QMAX, NT>(c, &sh, dsm, a);
+  const int64_t b = blockIdx.x / a.cs;
+  const int64_t r0 = (int64_t)c.rank * c.rpc;
+  const int64_t m = a.op.m;
+  const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, m - r0));
+  const cplx *Y = reinterpret_cast<const cplx *>(a.Y) + b * a.y_stride;
+  cplx *Cs = reinterpret_cast<cplx *>(c.Cs);
+  for (int e = c.tid; e < nloc * a.q; e += NT) {
+    int j = e / nloc, i = e % nloc;
+    Cs[(size_t)i * c.qp + j] = Y[(int64_t)j * a.ldy + r0 + i];
+  }
+  __syncthreads();
+  MVOut o;
+  const bool ok = maxvol_complex(c, m, sh.Isl, a.cap, o);
+  __syncthreads();
+  if (c.rank == 0) {
+    if (c.tid < a.q) a.I[b * a.q + c.tid] = sh.Isl[c.tid];
+    if (c.tid == 0) {
+      a.yinfo[4 * b + 0] = ok ? LRA_OK : LRA_ESINGULAR;
+      a.yinfo[4 * b + 1] = o.swaps;
+      a.yinfo[4 * b + 2] = o.cap_hit;
+      a.yinfo[4 * b + 3] = o.lu_steps;
+    }
+  }
+  cluster_barrier(c);
+}
+
+// ------------------------------------------------------------------ the C-A kernel
+// Steps: 0 = stage 2 on a real Y (cold); then 2L+1 = horizontal step of loop L
+// (J <- maxvol(W[I,:]^T), cold in loop 0), 2L+2 = vertical step (I <- maxvol(W[:,J]), warm).
+template <int Q, int TPR, int NT, int OPK>
+__global__ void __launch_bounds__(NT, 1) k_ca(CAArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ CAShared sh;
+  Ctx c;
+  ctx_init<Q, NT>(c, &sh, dsm, a);
   const int64_t b = blockIdx.x / a.cs;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE)
     op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int q = a.q;
   int32_t status = LRA_OK;
-  int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0;
+  int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0, sw_h = 0;
   double cert_r = 0.0, cert_c = 0.0;
-  MVOut o;
-  bool ok = true;
-
-  // stage 2: I <- maxvol(Y), or the given I0
-  if (a.Y) {
-    const char *Yb = (const char *)a.Y + b * a.y_stride * esz;
-    if (a.y_complex) {
-      load_Y<cplx>(c, Yb, a.ldy, op.m);
-      ok = maxvol_cold<cplx>(c, op.m, sh.Isl, a.cap, o);
-    } else {
-      load_Y<double>(c, Yb, a.ldy, op.m);
-      ok = maxvol_cold<double>(c, op.m, sh.Isl, a.cap, o);
-    }
-    if (ok) { lu += o.lu_steps; swaps += o.swaps; caps += o.cap_hit; sk_swaps = o.swaps; }
-  } else {
+  const int64_t r0 = (int64_t)c.rank * c.rpc;
+  const bool yreal = a.Y != nullptr && !a.y_complex;
+  if (!yreal) {
     if (c.tid < q) sh.Isl[c.tid] = a.I0[b * a.i0_stride + c.tid];
+    if (a.yinfo) {
+      status = a.yinfo[4 * b + 0];
+      swaps = sk_swaps = a.yinfo[4 * b + 1];
+      caps = a.yinfo[4 * b + 2];
+      lu = a.yinfo[4 * b + 3];
+    }
     __syncthreads();
   }
-  // stage 3: C-A loops
-  for (int loop = 0; ok && loop < a.sweeps; ++loop) {
-    cluster_barrier(c);              // nobody still reads the previous block
-    load_rowsT(c, op, sh.Isl, op.n);
-    if (loop == 0) {
-      __syncthreads();
-      ok = maxvol_cold<double>(c, op.n, sh.Jsl, a.cap, o);
-    } else {
-      ok = maxvol_warm(c, op.n, sh.Jsl, a.cap, o);
+  const double *Y = yreal ? reinterpret_cast<const double *>(a.Y) + b * a.y_stride : nullptr;
+  const int last = 2 * a.sweeps;
+  long long _tk = clock64();
+  for (int step = yreal ? 0 : 1; status == LRA_OK && step <= last; ++step) {
+    const int kind = step == 0 ? 0 : ((step & 1) ? 1 : 2);        // 0 = Y, 1 = h, 2 = v
+    const int64_t N = kind == 1 ? op.n : op.m;
+    long long *S = kind == 1 ? sh.Jsl : sh.Isl;
+    const bool cold = step <= 1;
+    cluster_barrier(c);                                             // previous block no longer read
+    CA_T0();
+    {
+      const int nloc = (int)max((int64_t)0, min((int64_t)c.rpc, N - r0));
+      const long long *I = sh.Isl, *J = sh.Jsl;
+      load_rows<TPR>(c, nloc, [&](int i, int j) -> double {
+        if (kind == 0) return __ldg(Y + (int64_t)j * a.ldy + r0 + i);
+        if (kind == 1) return op_at<OPK>(op, I[j], r0 + i);
+        return op_at<OPK>(op, r0 + i, J[j]);
+      });
     }
-    if (!ok) break;
-    const int sw_h = o.swaps;
-    lu += o.lu_steps; swaps += o.swaps; caps += o.cap_hit; cert_c = o.cert;
-    cluster_barrier(c);
-    load_cols(c, op, sh.Jsl, op.m);
-    ok = maxvol_warm(c, op.m, sh.Isl, a.cap, o);
-    if (!ok) break;
-    lu += o.lu_steps; swaps += o.swaps; caps += o.cap_hit; cert_r = o.cert;
-    ++loops;
-    if (loop > 0 && sw_h == 0 && o.swaps == 0) break;
+    __syncthreads();
+    CA_T1(0);
+    MVOut o;
+    if (!maxvol_real<Q, TPR>(c, N, S, cold, step >= 2, a.cap, o)) {
+      status = LRA_ESINGULAR;
+      break;
+    }
+    lu += o.lu_steps;
+    swaps += o.swaps;
+    caps += o.cap_hit;
+    if (kind == 0) sk_swaps = o.swaps;
+    if (kind == 1) { cert_c = o.cert; sw_h = o.swaps; }
+    if (kind == 2) {
+      cert_r = o.cert;
+      ++loops;
+      if (step > 2 && sw_h == 0 && o.swaps == 0) break;           // fixed point (reading C13)
+    }
   }
-  if (!ok) status = LRA_ESINGULAR;
+  __syncthreads();
+  if (threadIdx.x == 0 && c.rank == 0) atomicAdd(&g_ca_cyc[6], (unsigned long long)(clock64() - _tk));
   if (c.rank == 0) {
     if (c.tid < q) {
       a.I[b * q + c.tid] = sh.Isl[c.tid];
@@ -487,54 +955,94 @@ __global__ void __launch_bounds__(LRA_NT, 1) k_ca(CAArgs a) {
   cluster_barrier(c);                // keep every CTA's shared memory alive until done
 }
 
-size_t ca_smem_bytes(int rpc, int qp, int q, bool cplx) {
+static size_t ca_smem_bytes(int rpc, int qp, int q, int Q, bool cplx) {
   const size_t esz = cplx ? 16 : 8;
   size_t off = (size_t)rpc * qp * esz;
   off = (off + 15) & ~(size_t)15;
-  size_t lsz = (size_t)q * q * 8, lsz2 = (size_t)q * (q - 1) / 2 * esz;
-  off += lsz > lsz2 ? lsz : lsz2;
-  off = (off + 15) & ~(size_t)15;
-  off += (size_t)q * 16 + (size_t)rpc * 8 + (size_t)rpc;
+  off += cplx ? (size_t)q * (q - 1) / 2 * 16 : (size_t)q * 3 * Q * 8;
+  off += (size_t)rpc * 8 + (size_t)rpc;
   return (off + 15) & ~(size_t)15;
 }
 
-// Choose the smallest cluster size whose shared memory holds the block.
-cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
-  const bool cplx = a.y_complex != 0;
-  const size_t limit = 227 * 1024 - sizeof(CAShared) - 256;
-  int cs = 1;
-  int rpc = 0;
-  for (cs = 1; cs <= 16; cs *= 2) {
-    rpc = (int)((maxN + cs - 1) / cs);
-    if (ca_smem_bytes(rpc, a.qp, a.q, cplx) <= limit) break;
-  }
-  if (cs > 16) return cudaErrorInvalidConfiguration;
-  a.cs = cs;
-  a.rpc = rpc;
-  if (cs_out) *cs_out = cs;
-  const size_t smem = ca_smem_bytes(rpc, a.qp, a.q, cplx);
-  cudaError_t e = cudaFuncSetAttribute(k_ca, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <typename K>
+static cudaError_t launch_cluster(K kern, const CAArgs &a, int64_t nb, int nt, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (cs > 8) {
-    e = cudaFuncSetAttribute(k_ca, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (a.cs > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(nb * cs));
-  cfg.blockDim = dim3(LRA_NT);
+  cfg.gridDim = dim3((unsigned)(nb * a.cs));
+  cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.x = a.cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+static bool pick_cluster(int64_t maxN, int nt, int qp, int q, int Q, bool cplx, int &cs, int &rpc) {
+  const size_t limit = 227 * 1024 - sizeof(CAShared) - 256;
+  for (cs = 1; cs <= 16; cs *= 2) {
+    rpc = (int)((maxN + cs - 1) / cs);
+    if (rpc <= nt && ca_smem_bytes(rpc, qp, q, Q, cplx) <= limit) return true;
+  }
+  return false;
+}
+
+template <int Q, int TPR, int NT>
+static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
+  cudaError_t e;
+  if (a.y_complex) {                         // stage 2 on the complex sketch: own launch
+    CAArgs y = a;
+    if (!pick_cluster(a.op.m, 512, a.qp, a.q, LRA_QMAX, true, y.cs, y.rpc)) return cudaErrorInvalidConfiguration;
+    pf->begin("k_ca_ycplx", st);
+    e = launch_cluster(k_ca_ycplx<512>, y, nb, 512, ca_smem_bytes(y.rpc, y.qp, y.q, LRA_QMAX, true), st);
+    pf->end(st);
+    if (e != cudaSuccess) return e;
+    a.I0 = a.I;
+    a.i0_stride = a.q;
+  }
+  int cs, rpc;
+  if (!pick_cluster(maxN, NT / TPR, a.qp, a.q, Q, false, cs, rpc)) return cudaErrorInvalidConfiguration;
+  a.cs = cs;
+  a.rpc = rpc;
+  if (cs_out) *cs_out = cs;
+  CAArgs r = a;
+  r.y_complex = 0;
+  if (a.y_complex) r.Y = nullptr;
+  const size_t smem = ca_smem_bytes(rpc, a.qp, a.q, Q, false);
   pf->begin("k_ca", st);
-  e = cudaLaunchKernelEx(&cfg, k_ca, a);
+  if (a.op.kind == LRA_OP_FACTORED_CSR) e = launch_cluster(k_ca<Q, TPR, NT, 2>, r, nb, NT, smem, st);
+  else if (a.op.dtype == LRA_F64) e = launch_cluster(k_ca<Q, TPR, NT, 1>, r, nb, NT, smem, st);
+  else e = launch_cluster(k_ca<Q, TPR, NT, 0>, r, nb, NT, smem, st);
   pf->end(st);
   return e;
+}
+
+cudaError_t read_ca_counters(unsigned long long *out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_ca_cyc, sizeof(g_ca_cyc));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[16] = {0};
+    e = cudaMemcpyToSymbol(g_ca_cyc, z, sizeof(z));
+  }
+  return e;
+}
+
+cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
+  // (Q, threads per row, CTA threads): W = Q/TPR doubles of the row per lane
+  if (a.q <= 8) return launch_ca_t<8, 1, 512>(a, nb, maxN, st, cs_out, pf);
+  if (a.q <= 16) return launch_ca_t<16, 1, 512>(a, nb, maxN, st, cs_out, pf);
+  if (a.q <= 24) return launch_ca_t<24, 1, 512>(a, nb, maxN, st, cs_out, pf);
+  if (a.q <= 32) return launch_ca_t<32, 2, 512>(a, nb, maxN, st, cs_out, pf);
+  if (a.q <= 48) return launch_ca_t<48, 2, 512>(a, nb, maxN, st, cs_out, pf);
+  return launch_ca_t<64, 2, 512>(a, nb, maxN, st, cs_out, pf);
 }
 
 }  // namespace lra

@@ -61,8 +61,10 @@ struct CAArgs {
   int64_t *I, *J;              // outputs, stride q per problem
   lra_ca_stats *stats;         // per problem, may be null
   int32_t *status;             // per problem
+  int32_t *yinfo;              // per problem x4: complex stage-2 result (scratch), or null
 };
 cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
+cudaError_t read_ca_counters(unsigned long long *out, bool reset);
 
 struct NucArgs {
   OpView op;

@@ -32,8 +32,13 @@ static lra_status fail(lra_status s, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(LRA_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));   \
   } while (0)
 
+#define LRA_NSIDE 3
 struct lra_handle_s {
   int device;
+  int groups;                     // lra_batch groups (env LRA_BATCH_GROUPS, default 4)
+  cudaStream_t side[LRA_NSIDE];
+  cudaEvent_t fork, join[LRA_NSIDE];
+  bool streams_ready;
   int nranks, rank;
   int64_t launches;
   Prof prof;
@@ -41,6 +46,17 @@ struct lra_handle_s {
   void *ws;
   size_t ws_bytes;
 };
+
+static lra_status ensure_streams(lra_handle h) {
+  if (h->streams_ready) return LRA_OK;
+  for (int i = 0; i < LRA_NSIDE; ++i) {
+    CK(cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->join[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
+  h->streams_ready = true;
+  return LRA_OK;
+}
 
 static lra_status ws_reserve(lra_handle h, size_t bytes) {
   if (bytes <= h->ws_bytes) return LRA_OK;
@@ -172,6 +188,9 @@ lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_
   CK(cudaSetDevice(device));
   lra_handle_s *p = new lra_handle_s();
   p->device = device;
+  const char *g = getenv("LRA_BATCH_GROUPS");
+  p->groups = g ? atoi(g) : 4;
+  if (p->groups < 1) p->groups = 1;
   p->nranks = nranks;
   p->rank = rank;
   *h = p;
@@ -182,6 +201,13 @@ void lra_handle_destroy(lra_handle h) {
   if (!h) return;
   if (h->ws) cudaFree(h->ws);
   for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
+  if (h->streams_ready) {
+    for (int i = 0; i < LRA_NSIDE; ++i) {
+      cudaStreamDestroy(h->side[i]);
+      cudaEventDestroy(h->join[i]);
+    }
+    cudaEventDestroy(h->fork);
+  }
   delete h;
 }
 
@@ -221,6 +247,12 @@ int lra_profile_read(lra_handle h, int cap, const char **names, double *ms, int6
 
 int64_t lra_launch_count(lra_handle h) { return h ? h->launches : 0; }
 
+lra_status lra_debug_counters(uint64_t *out8, int reset) {
+  if (!out8 /* 16 entries */) return fail(LRA_EINVAL, "null output");
+  CK(read_ca_counters((unsigned long long *)out8, reset != 0));
+  return LRA_OK;
+}
+
 lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multiplier *M, void *Y, int64_t ldy,
                           void *stream) {
   lra_status s;
@@ -249,8 +281,8 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
                             int64_t y_stride, int y_complex, const int64_t *I0, int64_t r, int64_t k,
                             int32_t sweeps, double tol, double tau, int32_t cap, int64_t *I, int64_t *J,
                             double *U, double *A, double *B, int64_t a_stride, int64_t b_stride,
-                            lra_ca_stats *stats, int32_t *status, double *TS, double *Sr, int64_t nb,
-                            cudaStream_t st) {
+                            lra_ca_stats *stats, int32_t *status, double *TS, double *Sr, int32_t *yinfo,
+                            int64_t nb, cudaStream_t st) {
   CAArgs ca{};
   ca.op = make_view(W);
   ca.w_stride = w_stride;
@@ -270,6 +302,7 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   ca.J = J;
   ca.stats = stats;
   ca.status = status;
+  ca.yinfo = y_complex ? yinfo : nullptr;
   int cs = 0;
   cudaError_t e = launch_ca(ca, nb, W->m > W->n ? W->m : W->n, st, &cs, &h->prof);
   if (e == cudaErrorInvalidConfiguration)
@@ -330,6 +363,7 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
     probe.take<int32_t>(1);
     probe.take<double>((size_t)k * r);
     probe.take<double>((size_t)k * r);
+    probe.take<int32_t>(4);
     need = probe.off + 256;
   }
   if ((s = ws_reserve(h, need)) != LRA_OK) return s;
@@ -337,10 +371,11 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
   int32_t *status = cv.take<int32_t>(1);
   double *TS = cv.take<double>((size_t)k * r);
   double *Sr = cv.take<double>((size_t)k * r);
+  int32_t *yinfo = cv.take<int32_t>(4);
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
-  s = run_chain(h, W, 0, Y, ldy, 0, y_complex, I0, r, k, sweeps, swap_tol, tie_slack, swap_cap, I, J, U, A, B, 0,
-                0, stats, status, TS, Sr, 1, st);
+  s = run_chain(h, W, 0, Y, ldy, 0, y_complex, Y ? nullptr : I0, r, k, sweeps, swap_tol, tie_slack, swap_cap, I, J,
+                U, A, B, 0, 0, stats, status, TS, Sr, yinfo, 1, st);
   return s;
 }
 
@@ -411,6 +446,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   probe.take<double>((size_t)nb * m * r);
   probe.take<double>((size_t)nb * r * n);
   probe.take<double2>((size_t)nb * tiles);
+  probe.take<int32_t>((size_t)nb * 4);
   if ((s = ws_reserve(h, probe.off + 256)) != LRA_OK) return s;
   Carve cv{(char *)h->ws, 0};
   int32_t *status = cv.take<int32_t>(nb);
@@ -420,38 +456,62 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   double *A = cv.take<double>((size_t)nb * m * r);
   double *B = cv.take<double>((size_t)nb * r * n);
   double2 *part = cv.take<double2>((size_t)nb * tiles);
+  int32_t *yinfo = cv.take<int32_t>((size_t)nb * 4);
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, st));
-  // stage 1 for all blocks
-  SketchArgs sa = make_sketch(W0, M0, Y, m);
-  sa.w_stride = w_stride;
-  sa.m_stride = m_stride;
-  sa.y_stride = m * k;
-  if (M0->kind == LRA_MUL_GAUSSIAN) sa.m_stride = 0;
-  CK(launch_sketch(sa, nb, M0->omega, M0->ld_omega, st, &h->prof));
-  h->launches += 1;
-  // stages 2-3, nucleus, factors
-  s = run_chain(h, W0, w_stride, Y, m, m * k, cplx ? 1 : 0, nullptr, r, k, sweeps, swap_tol, tie_slack, swap_cap, I,
-                J, U, A, B, m * r, r * n, stats, status, TS, Sr, nb, st);
-  if (s != LRA_OK) return s;
-  // a-posteriori check per block
-  ResArgs ra{};
-  ra.dtype = W0->dtype;
-  ra.m = m;
-  ra.n = n;
-  ra.ldw = W0->ldw;
-  ra.w_stride = w_stride;
-  ra.w = W0->w;
-  ra.A = A;
-  ra.B = B;
-  ra.a_stride = m * r;
-  ra.b_stride = r * n;
-  ra.r = (int)r;
-  ra.partial = part;
-  ra.status = status;
-  int nl = 0;
-  CK(launch_residual(ra, nb, num2, den2, st, &nl, &h->prof));
-  h->launches += nl;
+  // Blocks are processed in groups on the handle's side streams (fork/join on `stream` with
+  // events, so the call stays stream-ordered and graph-capturable): the latency-bound C-A
+  // and nucleus of one group overlap the bandwidth-bound sketch/residual of another.
+  if ((s = ensure_streams(h)) != LRA_OK) return s;
+  int64_t ngroups = nb < h->groups ? nb : h->groups;
+  const int64_t gsz = (nb + ngroups - 1) / ngroups;
+  ngroups = (nb + gsz - 1) / gsz;
+  CK(cudaEventRecord(h->fork, st));
+  for (int i = 0; i < LRA_NSIDE; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));
+  const size_t wsz = W0->dtype == LRA_F32 ? 4 : 8;
+  for (int64_t g = 0; g < ngroups; ++g) {
+    const int64_t b0 = g * gsz, gn = (nb - b0) < gsz ? (nb - b0) : gsz;
+    cudaStream_t gs = h->side[g % LRA_NSIDE];
+    lra_operand Wg = *W0;
+    Wg.w = (const char *)W0->w + b0 * w_stride * wsz;
+    lra_multiplier Mg = *M0;
+    if (m_stride) {
+      Mg.sp_row = M0->sp_row + b0 * m_stride;
+      Mg.sp_sign = M0->sp_sign + b0 * m_stride;
+    }
+    char *Yg = (char *)Y + (size_t)b0 * m * k * esz;
+    SketchArgs sa = make_sketch(&Wg, &Mg, Yg, m);
+    sa.w_stride = w_stride;
+    sa.m_stride = m_stride;
+    sa.y_stride = m * k;
+    CK(launch_sketch(sa, gn, Mg.omega, Mg.ld_omega, gs, &h->prof));
+    h->launches += 1;
+    s = run_chain(h, &Wg, w_stride, Yg, m, m * k, cplx ? 1 : 0, nullptr, r, k, sweeps, swap_tol, tie_slack, swap_cap,
+                  I + b0 * k, J + b0 * k, U ? U + b0 * k * k : nullptr, A + b0 * m * r, B + b0 * r * n, m * r, r * n,
+                  stats ? stats + b0 : nullptr, status + b0, TS + b0 * k * r, Sr + b0 * k * r, yinfo + 4 * b0, gn, gs);
+    if (s != LRA_OK) return s;
+    ResArgs ra{};
+    ra.dtype = W0->dtype;
+    ra.m = m;
+    ra.n = n;
+    ra.ldw = W0->ldw;
+    ra.w_stride = w_stride;
+    ra.w = Wg.w;
+    ra.A = A + b0 * m * r;
+    ra.B = B + b0 * r * n;
+    ra.a_stride = m * r;
+    ra.b_stride = r * n;
+    ra.r = (int)r;
+    ra.partial = part + b0 * tiles;
+    ra.status = status + b0;
+    int nl = 0;
+    CK(launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof));
+    h->launches += nl;
+  }
+  for (int i = 0; i < LRA_NSIDE; ++i) {
+    CK(cudaEventRecord(h->join[i], h->side[i]));
+    CK(cudaStreamWaitEvent(st, h->join[i], 0));
+  }
   return LRA_OK;
 }
 

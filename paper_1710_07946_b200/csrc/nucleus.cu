@@ -11,8 +11,7 @@
 
 namespace lra {
 
-constexpr int NUC_NT = 256;
-constexpr int NUC_W = NUC_NT / 32;
+constexpr int NUC_NT = 1024;   // max threads; launched with 32 x (l/2) so each pair has a warp
 
 
 __device__ __forceinline__ void rr_pair(int L, int round, int i, int &a, int &b) {
@@ -27,6 +26,7 @@ __device__ __forceinline__ void rr_pair(int L, int round, int i, int &a, int &b)
 }
 
 __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
+  const int NT = blockDim.x, NW = NT >> 5;
   extern __shared__ __align__(16) double nsm[];
   const int64_t b = blockIdx.x;
   if (a.status[b] != LRA_OK) return;
@@ -42,19 +42,21 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int64_t *I = a.I + b * k, *J = a.J + b * l;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < L * k; e += NUC_NT) {
+  for (int e = tid; e < L * k; e += NT) {
     int j = e / k, i = e % k;
     G[e] = j < l ? op.at(I[i], J[j]) : 0.0;
   }
-  for (int e = tid; e < L * L; e += NUC_NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
+  for (int e = tid; e < L * L; e += NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
   __syncthreads();
-  const double eps = 1e-15;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  // rotate while cos(angle) between two columns exceeds 4·k·eps: the fp64 dot products of
+  // already-orthogonal columns carry relative errors ~k·eps, so a tighter test never stops
+  const double eps = 4.0 * (double)k * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
     int rot = 0;
     for (int round = 0; round < L - 1; ++round) {
-      for (int pi = warp; pi < L / 2; pi += NUC_W) {
+      for (int pi = warp; pi < L / 2; pi += NW) {
         int p, qq;
         rr_pair(L, round, pi, p, qq);
         double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
     if (!s_rot) break;
   }
   // singular values, descending order (ties: lower column first)
-  for (int j = warp; j < L; j += NUC_W) {
+  for (int j = warp; j < L; j += NW) {
     double s = 0.0;
     for (int i = lane; i < k; i += 32) s = fma(G[(size_t)j * ldg + i], G[(size_t)j * ldg + i], s);
     s = warp_sum(s);
@@ -112,12 +114,12 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   __syncthreads();
   if (a.status[b] != LRA_OK) return;
   double *TS = a.TS + b * (int64_t)l * r, *Sr = a.Sr + b * (int64_t)k * r;
-  for (int e = tid; e < l * r; e += NUC_NT) {      // TS[j, t] = T[j, ord t] / sigma
+  for (int e = tid; e < l * r; e += NT) {      // TS[j, t] = T[j, ord t] / sigma
     int t = e / l, j = e % l;
     int c = ord[t];
     TS[(size_t)t * l + j] = V[(size_t)c * L + j] / sig[c];
   }
-  for (int e = tid; e < k * r; e += NUC_NT) {      // Sr[i, t] = G[i, ord t] / sigma
+  for (int e = tid; e < k * r; e += NT) {      // Sr[i, t] = G[i, ord t] / sigma
     int t = e / k, i = e % k;
     int c = ord[t];
     Sr[(size_t)t * k + i] = G[(size_t)c * ldg + i] / sig[c];
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   __syncthreads();
   if (a.U) {
     double *U = a.U + b * (int64_t)l * k;
-    for (int e = tid; e < l * k; e += NUC_NT) {    // U (l x k, col-major) = TS * Sr^T
+    for (int e = tid; e < l * k; e += NT) {    // U (l x k, col-major) = TS * Sr^T
       int col = e / l, row = e % l;
       double s = 0.0;
       for (int t = 0; t < r; ++t) s = fma(TS[(size_t)t * l + row], Sr[(size_t)t * k + col], s);
@@ -214,7 +216,9 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   cudaError_t e = cudaFuncSetAttribute(k_nucleus, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   pf->begin("k_nucleus", st);
-  k_nucleus<<<(unsigned)nb, NUC_NT, smem, st>>>(na);
+  const int L = (na.l + 1) & ~1;
+  const int nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
+  k_nucleus<<<(unsigned)nb, nt, smem, st>>>(na);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   dim3 gA((unsigned)((fa.op.m + 63) / 64), (unsigned)nb);

@@ -79,6 +79,8 @@ def _load():
     lib.lra_profile_enable.restype = C.c_int
     lib.lra_profile_read.argtypes = [vp, C.c_int, P(C.c_char_p), P(C.c_double), P(i64)]
     lib.lra_profile_read.restype = C.c_int
+    lib.lra_debug_counters.argtypes = [P(C.c_uint64), C.c_int]
+    lib.lra_debug_counters.restype = C.c_int
     for f in ("lra_handle_create", "lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
         getattr(lib, f).restype = C.c_int
     return lib
@@ -96,7 +98,15 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read"]
+            "lra_profile_read", "lra_debug_counters"]
+
+
+def debug_counters(reset=True):
+    out = (C.c_uint64 * 16)()
+    _check(lib().lra_debug_counters(out, int(reset)))
+    names = ["load", "cold_lu", "warm_gather", "gauss_jordan", "product", "swap_loop", "kernel", "pivot_steps",
+             "sw_ctamax", "sw_ctaidx", "sw_pub", "x_barrier", "x_triples", "x_prow", "sw_update", "-"]
+    return dict(zip(names, [int(x) for x in out]))
 
 
 def _check(st):
