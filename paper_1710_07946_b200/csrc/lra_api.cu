@@ -35,7 +35,7 @@ static lra_status fail(lra_status s, const char *fmt, ...) {
 #define LRA_NSIDE 3
 struct lra_handle_s {
   int device;
-  int groups;                     // lra_batch groups (env LRA_BATCH_GROUPS, default 4)
+  int groups;                     // lra_batch groups (env LRA_BATCH_GROUPS, default 2)
   cudaStream_t side[LRA_NSIDE];
   cudaEvent_t fork, join[LRA_NSIDE];
   bool streams_ready;
@@ -189,7 +189,7 @@ lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_
   lra_handle_s *p = new lra_handle_s();
   p->device = device;
   const char *g = getenv("LRA_BATCH_GROUPS");
-  p->groups = g ? atoi(g) : 4;
+  p->groups = g ? atoi(g) : 2;
   if (p->groups < 1) p->groups = 1;
   p->nranks = nranks;
   p->rank = rank;

@@ -16,39 +16,22 @@ constexpr int RS_KC = 16;    // k-chunk
 constexpr int RS_NT = 256;
 
 
-template <typename TW>
-__device__ __forceinline__ void ld8(const TW *p, bool vec, int rows_left, double v[8]);
-template <>
-__device__ __forceinline__ void ld8<float>(const float *p, bool vec, int rows_left, double v[8]) {
-  if (vec && rows_left >= 8) {
-    float4 a = __ldcs(reinterpret_cast<const float4 *>(p));
-    float4 b = __ldcs(reinterpret_cast<const float4 *>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int x = 0; x < 8; ++x) v[x] = x < rows_left ? (double)p[x] : 0.0;
-  }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
-template <>
-__device__ __forceinline__ void ld8<double>(const double *p, bool vec, int rows_left, double v[8]) {
-  if (vec && rows_left >= 8) {
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      double2 a = __ldcs(reinterpret_cast<const double2 *>(p) + x);
-      v[2 * x] = a.x; v[2 * x + 1] = a.y;
-    }
-  } else {
-#pragma unroll
-    for (int x = 0; x < 8; ++x) v[x] = x < rows_left ? p[x] : 0.0;
-  }
-}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// grid: (tiles_m * tiles_n, nb)
+// grid: (tiles_m * tiles_n, nb).  Thread (tx, ty) owns rows tx + 16 i and columns ty*8 + j
+// (i, j < 8): the A-panel reads of a warp are 16 consecutive doubles (conflict-free) and the
+// W reads are 64-byte column segments.  For fp32 W the whole 128 x 128 tile is prefetched
+// into shared memory with cp.async at the start, overlapping the fp64 FMA loop.
 template <typename TW>
 __global__ void __launch_bounds__(RS_NT) k_residual(ResArgs a) {
   __shared__ __align__(16) double As[RS_KC][RS_T];
   __shared__ __align__(16) double Bs[RS_KC][RS_T];
   __shared__ double red[2][RS_NT / 32];
+  extern __shared__ __align__(16) float Wsm[];          // [RS_T cols][RS_T rows] (fp32 only)
   const int64_t b = blockIdx.y;
   const int64_t tile = blockIdx.x;
   if (a.status && a.status[b] != LRA_OK) return;
@@ -58,6 +41,17 @@ __global__ void __launch_bounds__(RS_NT) k_residual(ResArgs a) {
   const double *A = a.A + b * a.a_stride;
   const double *B = a.B + b * a.b_stride;
   const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
+  constexpr bool PRE = sizeof(TW) == 4;
+  const bool full = row0 + RS_T <= a.m && col0 + RS_T <= a.n && (a.ldw & 3) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
+  if (PRE && full) {
+    // 128 columns x 512 B, 16-byte chunks: chunk e -> column e / 32, rows 4 (e % 32) ..
+    for (int e = tid; e < RS_T * (RS_T / 4); e += RS_NT) {
+      const int col = e >> 5, r4 = (e & 31) * 4;
+      cp_async16(&Wsm[col * RS_T + r4], W + (col0 + col) * a.ldw + row0 + r4);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   double acc[8][8];
 #pragma unroll
   for (int x = 0; x < 8; ++x)
@@ -79,9 +73,9 @@ __global__ void __launch_bounds__(RS_NT) k_residual(ResArgs a) {
     for (int kk = 0; kk < RS_KC; ++kk) {
       double av[8], bv[8];
 #pragma unroll
+      for (int x = 0; x < 8; ++x) av[x] = As[kk][tx + 16 * x];
+#pragma unroll
       for (int x = 0; x < 4; ++x) {
-        double2 t = reinterpret_cast<const double2 *>(&As[kk][tx * 8])[x];
-        av[2 * x] = t.x; av[2 * x + 1] = t.y;
         double2 u = reinterpret_cast<const double2 *>(&Bs[kk][ty * 8])[x];
         bv[2 * x] = u.x; bv[2 * x + 1] = u.y;
       }
@@ -92,23 +86,34 @@ __global__ void __launch_bounds__(RS_NT) k_residual(ResArgs a) {
     }
     __syncthreads();
   }
-  // epilogue: stream the W tile once
-  const int64_t gi0 = row0 + tx * 8;
-  const int rows_left = (int)max((int64_t)0, min((int64_t)8, a.m - gi0));
-  const bool vec = ((a.ldw & 7) == 0) && ((reinterpret_cast<uintptr_t>(W) & 31) == 0);
   double num = 0.0, den = 0.0;
+  if (PRE && full) {
+    cp_async_wait_all();
+    __syncthreads();
 #pragma unroll
-  for (int y = 0; y < 8; ++y) {
-    const int64_t gj = col0 + ty * 8 + y;
-    if (gj < a.n && rows_left > 0) {
-      double wv[8];
-      ld8<TW>(W + gj * a.ldw + gi0, vec, rows_left, wv);
+    for (int y = 0; y < 8; ++y) {
+      const float *wc = &Wsm[(ty * 8 + y) * RS_T + tx];
 #pragma unroll
       for (int x = 0; x < 8; ++x) {
-        if (x < rows_left) {
-          const double d = wv[x] - acc[x][y];
+        const double w = (double)wc[16 * x];
+        const double d = w - acc[x][y];
+        num = fma(d, d, num);
+        den = fma(w, w, den);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const int64_t gj = col0 + ty * 8 + y;
+      if (gj >= a.n) continue;
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        const int64_t gi = row0 + tx + 16 * x;
+        if (gi < a.m) {
+          const double w = (double)W[gj * a.ldw + gi];
+          const double d = w - acc[x][y];
           num = fma(d, d, num);
-          den = fma(wv[x], wv[x], den);
+          den = fma(w, w, den);
         }
       }
     }
@@ -159,8 +164,14 @@ cudaError_t launch_residual(ResArgs a, int64_t nb, double *num2, double *den2, c
   a.tiles_n = (a.n + RS_T - 1) / RS_T;
   dim3 grid((unsigned)(a.tiles_m * a.tiles_n), (unsigned)nb);
   pf->begin("k_residual", st);
-  if (a.dtype == LRA_F32) k_residual<float><<<grid, RS_NT, 0, st>>>(a);
-  else k_residual<double><<<grid, RS_NT, 0, st>>>(a);
+  if (a.dtype == LRA_F32) {
+    const int sm = RS_T * RS_T * 4;
+    cudaError_t e0 = cudaFuncSetAttribute(k_residual<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e0 != cudaSuccess) return e0;
+    k_residual<float><<<grid, RS_NT, sm, st>>>(a);
+  } else {
+    k_residual<double><<<grid, RS_NT, 0, st>>>(a);
+  }
   pf->end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

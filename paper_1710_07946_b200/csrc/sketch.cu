@@ -95,22 +95,39 @@ __global__ void __launch_bounds__(SK_NT) k_sketch_structured(SketchArgs a) {
   const int64_t left = a.m - i0;
   const bool vec = ((a.ldw & 3) == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
   double accr[4] = {0.0, 0.0, 0.0, 0.0}, acci[4] = {0.0, 0.0, 0.0, 0.0};
-  // loads of up to 8 terms in flight before the ordered accumulation
-  for (int t0 = 0; t0 < T; t0 += 8) {
-    double v[8][4];
+  // all loads of a 16-term chunk in flight (raw TW values), then the ordered accumulation
+  constexpr int CH = sizeof(TW) == 4 ? 16 : 8;
+  for (int t0 = 0; t0 < T; t0 += CH) {
+    TW v[CH][4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (t0 + u < T) load4<TW>(W + s_k[t0 + u] * a.ldw + i0, vec, left, v[u]);
+    for (int u = 0; u < CH; ++u) {
+      if (t0 + u < T) {
+        const TW *src = W + s_k[t0 + u] * a.ldw + i0;
+        if (vec && left >= 4) {
+          if (sizeof(TW) == 4) {
+            float4 f = __ldcs(reinterpret_cast<const float4 *>(src));
+            v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w;
+          } else {
+            double2 d0 = __ldcs(reinterpret_cast<const double2 *>(src));
+            double2 d1 = __ldcs(reinterpret_cast<const double2 *>(src) + 1);
+            v[u][0] = d0.x; v[u][1] = d0.y; v[u][2] = d1.x; v[u][3] = d1.y;
+          }
+        } else {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+          for (int r = 0; r < 4; ++r) v[u][r] = r < left ? src[r] : (TW)0;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
       if (t0 + u < T) {
         const double cr = s_cr[t0 + u];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) accr[r] = __dadd_rn(accr[r], __dmul_rn(cr, v[u][r]));
+        for (int r = 0; r < 4; ++r) accr[r] = __dadd_rn(accr[r], __dmul_rn(cr, (double)v[u][r]));
         if (CPLX) {
           const double ci = s_ci[t0 + u];
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acci[r] = __dadd_rn(acci[r], __dmul_rn(v[u][r], ci));
+          for (int r = 0; r < 4; ++r) acci[r] = __dadd_rn(acci[r], __dmul_rn((double)v[u][r], ci));
         }
       }
     }
@@ -122,9 +139,14 @@ __global__ void __launch_bounds__(SK_NT) k_sketch_structured(SketchArgs a) {
       if (r < left) Y[i0 + r] = make_double2(accr[r], acci[r]);
   } else {
     double *Y = reinterpret_cast<double *>(a.y) + b * a.y_stride + (int64_t)c * a.ldy;
+    if (left >= 4 && ((reinterpret_cast<uintptr_t>(Y + i0) & 15) == 0)) {
+      reinterpret_cast<double2 *>(Y + i0)[0] = make_double2(accr[0], accr[1]);
+      reinterpret_cast<double2 *>(Y + i0)[1] = make_double2(accr[2], accr[3]);
+    } else {
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      if (r < left) Y[i0 + r] = accr[r];
+      for (int r = 0; r < 4; ++r)
+        if (r < left) Y[i0 + r] = accr[r];
+    }
   }
 }
 
