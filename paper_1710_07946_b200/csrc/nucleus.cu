@@ -48,41 +48,74 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   }
   for (int e = tid; e < L * L; e += NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
   __syncthreads();
-  // rotate while cos(angle) between two columns exceeds 4·k·eps: the fp64 dot products of
-  // already-orthogonal columns carry relative errors ~k·eps, so a tighter test never stops
+  // One-sided (Hestenes) Jacobi, Rutishauser's rotation.  Column norms are cached and
+  // updated analytically (a_pp' = a_pp - t a_pq, a_qq' = a_qq + t a_pq), refreshed from
+  // the data at every sweep, so a pair costs one dot product; the rotation uses
+  // reciprocal / rsqrt instead of IEEE divisions and square roots.  Rotate while
+  // cos(angle) between two columns exceeds 4·k·eps (the fp64 dot products of already
+  // orthogonal columns carry relative errors ~k·eps, so a tighter test never stops).
+  double *nrm = sig;                   // cached squared column norms (L)
+  __shared__ unsigned char s_pair[63 * 32 * 2];   // round-robin schedule (L <= 64)
+  for (int e = tid; e < (L - 1) * (L / 2); e += NT) {
+    int p, qq;
+    rr_pair(L, e / (L / 2), e % (L / 2), p, qq);
+    s_pair[2 * e] = (unsigned char)p;
+    s_pair[2 * e + 1] = (unsigned char)qq;
+  }
   const double eps = 4.0 * (double)k * 2.220446049250313e-16;
+  const double eps2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
+    for (int j = warp; j < L; j += NW) {
+      double s2 = 0.0;
+      for (int i = lane; i < k; i += 32) s2 = fma(G[(size_t)j * ldg + i], G[(size_t)j * ldg + i], s2);
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
     if (tid == 0) s_rot = 0;
     __syncthreads();
     int rot = 0;
     for (int round = 0; round < L - 1; ++round) {
       for (int pi = warp; pi < L / 2; pi += NW) {
-        int p, qq;
-        rr_pair(L, round, pi, p, qq);
+        const int p = s_pair[2 * (round * (L / 2) + pi)], qq = s_pair[2 * (round * (L / 2) + pi) + 1];
         double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < k; i += 32) {
-          al = fma(gp[i], gp[i], al);
-          be = fma(gq[i], gq[i], be);
-          ga = fma(gp[i], gq[i], ga);
+        double xv[2], yv[2];
+        double ga = 0.0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = lane + 32 * u;
+          xv[u] = i < k ? gp[i] : 0.0;
+          yv[u] = i < k ? gq[i] : 0.0;
+          ga = fma(xv[u], yv[u], ga);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
         ga = warp_sum(ga);
-        if (fabs(ga) > eps * sqrt(al * be) && ga != 0.0) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          for (int i = lane; i < k; i += 32) {
-            double x = gp[i], y = gq[i];
-            gp[i] = cs * x - sn * y;
-            gq[i] = sn * x + cs * y;
+        const double al = nrm[p], be = nrm[qq];
+        if (ga * ga > eps2 * al * be && ga != 0.0) {
+          const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
+          const double z2 = fma(zeta, zeta, 1.0);
+          const double h = z2 * rsqrt(z2);                       // sqrt(1 + zeta^2)
+          const double t = copysign(__drcp_rn(fabs(zeta) + h), zeta);
+          const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int i = lane + 32 * u;
+            if (i < k) {
+              gp[i] = cs * xv[u] - sn * yv[u];
+              gq[i] = sn * xv[u] + cs * yv[u];
+            }
           }
           double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
-          for (int i = lane; i < L; i += 32) {
-            double x = vp[i], y = vq[i];
-            vp[i] = cs * x - sn * y;
-            vq[i] = sn * x + cs * y;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int i = lane + 32 * u;
+            if (i < L) {
+              const double x = vp[i], y = vq[i];
+              vp[i] = cs * x - sn * y;
+              vq[i] = sn * x + cs * y;
+            }
+          }
+          if (lane == 0) {
+            nrm[p] = fma(-t, ga, al);
+            nrm[qq] = fma(t, ga, be);
           }
           rot = 1;
         }
