@@ -160,6 +160,9 @@ class DenseOperand:
     def block(self, I, J):
         return self.W[np.ix_(np.asarray(I), np.asarray(J))]
 
+    def entries(self, ii, jj):
+        return self.W[np.asarray(ii), np.asarray(jj)]
+
 
 class FactoredOperand:
     """Entry oracle W_ij = A_{i,:}·B_{:,j} + E_ij with E in CSR (config 4); W never formed."""
@@ -194,6 +197,19 @@ class FactoredOperand:
 
     def block(self, I, J):
         return self.rows(I)[:, np.asarray(J)]
+
+    def entries(self, ii, jj):
+        """W(i_q, j_q) = A[i_q,:]·B[:,j_q] + E(i_q, j_q) for arrays of pairs."""
+        ii = np.asarray(ii, dtype=np.int64)
+        jj = np.asarray(jj, dtype=np.int64)
+        w = np.einsum("qt,tq->q", self.A[ii, :], self.B[:, jj])
+        rows = np.repeat(np.arange(self.m, dtype=np.int64), np.diff(self.row_ptr))
+        keys = rows * self.n + self.col
+        qk = ii * self.n + jj
+        pos = np.searchsorted(keys, qk)
+        pos = np.minimum(pos, len(keys) - 1)
+        hit = keys[pos] == qk if len(keys) else np.zeros(len(qk), bool)
+        return w + np.where(hit, self.val[pos] if len(keys) else 0.0, 0.0)
 
 
 # ============================================================ C-A loops (stage 3)
@@ -293,8 +309,7 @@ def sampled_residual(op, A, B, ii, jj):
     """Sampled estimate num²_est = (mn/Q)·Σ_q d_q², d_q = W(i_q,j_q) − A[i_q,:]·B[:,j_q]
     over Q i.i.d. uniform pairs (the mn/Q extrapolation is SPEC S:280-288)."""
     Q = len(ii)
-    w = np.array([op.block([i], [j])[0, 0] for i, j in zip(ii, jj)]) if not isinstance(op, DenseOperand) \
-        else op.W[ii, jj]
+    w = op.entries(ii, jj)
     d = w - np.einsum("qt,tq->q", A[ii, :], B[:, jj])
     return op.m * op.n / Q * float(np.sum(d * d))
 

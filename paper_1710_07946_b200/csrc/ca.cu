@@ -80,16 +80,44 @@ struct Ctx {
   int ib;                      // column offset of the carried G^{-1} inside aug (0 or Q)
   int rb;                      // CTA reduction buffer parity
   double tau, tol;
+  // grid tier (one problem spread over the whole grid, cooperative launch): exchanges go
+  // through global memory instead of DSMEM
+  int grid;
+  Tri *gtri;                   // [2][cs]  CTA triples
+  double *grow;                // [2][cs][LRA_QMAX]  CTA candidate rows
+  double *gG;                  // [LRA_QMAX][LRA_QMAX]  rows B[S,:] for warm starts
 };
 
 __device__ __forceinline__ void cluster_barrier(const Ctx &c) {
-  if (c.cs > 1) cg::this_cluster().sync();
+  if (c.grid) cg::this_grid().sync();
+  else if (c.cs > 1) cg::this_cluster().sync();
   else __syncthreads();
+}
+// where this CTA publishes its candidate row for exchange parity p
+__device__ __forceinline__ double *pub_slot(const Ctx &c, int p) {
+  return c.grid ? c.grow + ((size_t)p * c.cs + c.rank) * LRA_QMAX : &c.sh->pub[p][0];
 }
 template <typename T>
 __device__ __forceinline__ T *remote(const Ctx &c, T *p, int rank) {
   if (c.cs == 1) return p;
   return cg::this_cluster().map_shared_rank(p, rank);
+}
+// grid tier: owners copy the block rows B[S[a],:] of their CTA to gG before the barrier
+__device__ __forceinline__ void publish_S_rows(const Ctx &c, const long long *S, int64_t r0, int nloc) {
+  if (!c.grid) return;
+  for (int a = c.warp; a < c.q; a += c.nw) {
+    const long long sr = S[a];
+    if (sr < r0 || sr >= r0 + nloc) continue;
+    const double *src = reinterpret_cast<const double *>(c.Cs) + (size_t)(sr - r0) * c.qp;
+    for (int e = c.lane; e < c.q; e += 32) __stcg(c.gG + (size_t)a * LRA_QMAX + e, src[e]);
+  }
+}
+// element e of B[S[a],:] after the barrier (DSMEM read in the cluster tier, L2 in the grid tier)
+__device__ __forceinline__ double S_row_elem(const Ctx &c, const long long *S, int a, int e) {
+  if (c.grid) return __ldcg(c.gG + (size_t)a * LRA_QMAX + e);
+  const long long sr = S[a];
+  const double *src = reinterpret_cast<const double *>(c.Cs) + (size_t)(sr % c.rpc) * c.qp;
+  return remote(c, src, (int)(sr / c.rpc))[e];
 }
 
 // ------------------------------------------------------ CTA reductions (1 barrier each)
@@ -148,23 +176,57 @@ __device__ Pick exchange(Ctx &c, int p, double Mc, long long idxc, double vc, in
   long long _tm = clock64();
   // push this CTA's triple into slot `rank` of every CTA (remote stores; ordered by the
   // cluster barrier's release/acquire), so the decision needs no remote load round trip
-  if (c.warp == 0 && c.lane < c.cs) *remote(c, &c.sh->xin[p][c.rank], c.lane) = Tri{Mc, idxc, vc};
+  if (c.grid) {
+    if (c.tid == 0) {
+      Tri *dst = c.gtri + (size_t)p * c.cs + c.rank;
+      __stcg(&dst->M, Mc);
+      __stcg(&dst->idx, idxc);
+      __stcg(&dst->v, vc);
+    }
+  } else if (c.warp == 0 && c.lane < c.cs) {
+    *remote(c, &c.sh->xin[p][c.rank], c.lane) = Tri{Mc, idxc, vc};
+  }
   cluster_barrier(c);
   CA_MARK(11);
   if (c.warp == 0) {
-    Tri t{-INFINITY, LLONG_MAX, 0.0};
-    if (c.lane < c.cs) t = c.sh->xin[p][c.lane];
-    const double M = __longlong_as_double((long long)warp_max_key(dkey(t.M)));
+    // per lane: the best of CTAs lane, lane+32, ... (grid tier: up to 148 CTAs)
+    double tM = -INFINITY;
+    long long tcand = LLONG_MAX;
+    int tamb = 0, twr = -1;
+    double Mloc = -INFINITY;
+    for (int r = c.lane; r < c.cs; r += 32) {
+      Tri t;
+      if (c.grid) {
+        const Tri *src = c.gtri + (size_t)p * c.cs + r;
+        t = Tri{__ldcg(&src->M), __ldcg(&src->idx), __ldcg(&src->v)};
+      } else {
+        t = c.sh->xin[p][r];
+      }
+      Mloc = fmax(Mloc, t.M);
+    }
+    const double M = __longlong_as_double((long long)warp_max_key(dkey(Mloc)));
     const double thr = (1.0 - c.tau) * M;
-    const long long cand = (t.M >= thr && t.v >= thr) ? t.idx : LLONG_MAX;
-    const int amb = __any_sync(0xffffffffu, c.lane < c.cs && t.M >= thr && t.v < thr);
-    const long long best = warp_min_ll(cand);
-    const int wr = __ffs(__ballot_sync(0xffffffffu, c.lane < c.cs && cand == best && best != LLONG_MAX)) - 1;
+    for (int r = c.lane; r < c.cs; r += 32) {
+      Tri t;
+      if (c.grid) {
+        const Tri *src = c.gtri + (size_t)p * c.cs + r;
+        t = Tri{__ldcg(&src->M), __ldcg(&src->idx), __ldcg(&src->v)};
+      } else {
+        t = c.sh->xin[p][r];
+      }
+      if (t.M >= thr && t.v >= thr && t.idx < tcand) { tcand = t.idx; twr = r; }
+      if (t.M >= thr && t.v < thr) tamb = 1;
+    }
+    (void)tM;
+    const int amb = __any_sync(0xffffffffu, tamb);
+    const long long best = warp_min_ll(tcand);
+    const int wl = __ffs(__ballot_sync(0xffffffffu, tcand == best && best != LLONG_MAX)) - 1;
+    const int wr = wl >= 0 ? __shfl_sync(0xffffffffu, twr, wl) : -1;
     if (!amb && wr >= 0) {
-      const double *src = remote(c, &c.sh->pub[p][0], wr);
+      const double *src = c.grid ? c.grow + ((size_t)p * c.cs + wr) * LRA_QMAX : remote(c, &c.sh->pub[p][0], wr);
       const int js = (mode == 2) ? (int)(best % c.q) : -1;
       for (int j = c.lane; j < nwords; j += 32) {
-        const double x = src[j];
+        const double x = c.grid ? __ldcg(src + j) : src[j];
         c.sh->prow[j] = x;
         if (mode == 1) c.sh->pm[j] = (j > arg) ? x : 0.0;
         if (mode == 2) {
@@ -459,8 +521,9 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
       int p = c.par;
       c.par ^= 1;
       if (has && grow == idx) {
+        double *pb = pub_slot(c, p);
 #pragma unroll
-        for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+        for (int w = 0; w < W; ++w) pb[jb + w] = row[w];
       }
       Pick pk = exchange(c, p, Mc, idx, v, Q, 1, t);
       if (!(pk.M > 0.0) || !isfinite(pk.M)) return false;
@@ -473,8 +536,9 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
         p = c.par;
         c.par ^= 1;
         if (has && grow == i2) {
+          double *pb = pub_slot(c, p);
 #pragma unroll
-          for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+          for (int w = 0; w < W; ++w) pb[jb + w] = row[w];
         }
         pk = exchange(c, p, pk.M, i2, v2, Q, 1, t);
       }
@@ -503,14 +567,12 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
     CA_T0();
     if (cold || !carried) {
       // ---- G = B[S,:] gathered from the owners' shared memory, G^{-1} by Gauss-Jordan
+      publish_S_rows(c, S, r0, nloc);
       cluster_barrier(c);                            // every CTA's block rows are loaded
       for (int a = c.warp; a < q; a += c.nw) {       // [G | I]
-        const long long sr = S[a];
-        const double *src = remote(c, reinterpret_cast<const double *>(c.Cs), (int)(sr / c.rpc)) +
-                            (size_t)(sr % c.rpc) * c.qp;
         for (int e = c.lane; e < 2 * Q; e += 32) {
           double xv;
-          if (e < Q) xv = (e < q) ? src[e] : 0.0;
+          if (e < Q) xv = (e < q) ? S_row_elem(c, S, a, e) : 0.0;
           else xv = (e - Q == a) ? 1.0 : 0.0;
           c.X[a * c.AS + e] = xv;
         }
@@ -534,13 +596,10 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
       const int cur = c.ib, pa = (cur + Q) % (3 * Q), pb = (cur + 2 * Q) % (3 * Q);
       for (int a = c.warp; a < q; a += c.nw)         // X0 = cur^T -> part pa
         for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + pa + e] = (e < q) ? c.X[e * c.AS + cur + a] : 0.0;
+      publish_S_rows(c, S, r0, nloc);
       cluster_barrier(c);                            // every CTA's block rows are loaded
-      for (int a = c.warp; a < q; a += c.nw) {       // G = B[S,:] -> part pb
-        const long long sr = S[a];
-        const double *src = remote(c, reinterpret_cast<const double *>(c.Cs), (int)(sr / c.rpc)) +
-                            (size_t)(sr % c.rpc) * c.qp;
-        for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + pb + e] = (e < q) ? src[e] : 0.0;
-      }
+      for (int a = c.warp; a < q; a += c.nw)         // G = B[S,:] -> part pb
+        for (int e = c.lane; e < Q; e += 32) c.X[a * c.AS + pb + e] = (e < q) ? S_row_elem(c, S, a, e) : 0.0;
       __syncthreads();
       mm_small(c, cur, pb, pa, -1, -1.0);            // R  = I - G X0   -> part cur
       mm_small(c, pb, pa, cur, pa, 1.0);             // X1 = X0 + X0 R  -> part pb
@@ -577,8 +636,9 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
     int p = c.par;
     c.par ^= 1;
     if (has && idx != LLONG_MAX && grow == idx / q) {
+      double *pb = pub_slot(c, p);
 #pragma unroll
-      for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+      for (int w = 0; w < W; ++w) pb[jb + w] = row[w];
     }
     CA_MARK(10);
     Pick pk = exchange(c, p, Mc, idx, v, Q, 2);
@@ -608,8 +668,9 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
       p = c.par;
       c.par ^= 1;
       if (has && i2 != LLONG_MAX && grow == i2 / q) {
+        double *pb = pub_slot(c, p);
 #pragma unroll
-        for (int w = 0; w < W; ++w) c.sh->pub[p][jb + w] = row[w];
+        for (int w = 0; w < W; ++w) pb[jb + w] = row[w];
       }
       pk = exchange(c, p, pk.M, i2, v2, Q, 2);
     }
@@ -817,6 +878,11 @@ __device__ __forceinline__ void ctx_init(Ctx &c, CAShared *sh, unsigned char *ds
   c.rb = 0;
   c.tau = a.tau;
   c.tol = a.tol;
+  c.grid = a.grid;
+  c.gtri = reinterpret_cast<Tri *>(a.gscratch);
+  c.grow = a.gscratch ? reinterpret_cast<double *>(c.gtri + 2 * (size_t)a.cs) : nullptr;
+  c.gG = a.gscratch ? c.grow + 2 * (size_t)a.cs * LRA_QMAX : nullptr;
+  if (a.grid) c.rank = blockIdx.x;
   const size_t esz = a.y_complex ? 16 : 8;
   size_t off = 0;
   c.Cs = dsm;
@@ -872,7 +938,7 @@ __global__ void __launch_bounds__(NT, 1) k_ca(CAArgs a) {
   __shared__ CAShared sh;
   Ctx c;
   ctx_init<Q, NT>(c, &sh, dsm, a);
-  const int64_t b = blockIdx.x / a.cs;
+  const int64_t b = a.grid ? 0 : blockIdx.x / a.cs;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE)
     op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
@@ -996,6 +1062,20 @@ static bool pick_cluster(int64_t maxN, int nt, int qp, int q, int Q, bool cplx, 
   return false;
 }
 
+size_t ca_grid_scratch_bytes(int cs) {
+  return (size_t)2 * cs * sizeof(Tri) + (size_t)2 * cs * LRA_QMAX * 8 + (size_t)LRA_QMAX * LRA_QMAX * 8 + 256;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 template <int Q, int TPR, int NT>
 static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
   cudaError_t e;
@@ -1010,20 +1090,64 @@ static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
     a.i0_stride = a.q;
   }
   int cs, rpc;
-  if (!pick_cluster(maxN, NT / TPR, a.qp, a.q, Q, false, cs, rpc)) return cudaErrorInvalidConfiguration;
-  a.cs = cs;
-  a.rpc = rpc;
-  if (cs_out) *cs_out = cs;
   CAArgs r = a;
   r.y_complex = 0;
   if (a.y_complex) r.Y = nullptr;
+  if (pick_cluster(maxN, NT / TPR, a.qp, a.q, Q, false, cs, rpc)) {   // cluster tier
+    r.cs = cs;
+    r.rpc = rpc;
+    r.grid = 0;
+    if (cs_out) *cs_out = cs;
+    const size_t smem = ca_smem_bytes(rpc, a.qp, a.q, Q, false);
+    pf->begin("k_ca", st);
+    if (a.op.kind == LRA_OP_FACTORED_CSR) e = launch_cluster(k_ca<Q, TPR, NT, 2>, r, nb, NT, smem, st);
+    else if (a.op.dtype == LRA_F64) e = launch_cluster(k_ca<Q, TPR, NT, 1>, r, nb, NT, smem, st);
+    else e = launch_cluster(k_ca<Q, TPR, NT, 0>, r, nb, NT, smem, st);
+    pf->end(st);
+    return e;
+  }
+  // grid tier: one problem over ceil(maxN / rows-per-CTA) co-resident CTAs (cooperative)
+  rpc = NT / TPR;
+  cs = (int)((maxN + rpc - 1) / rpc);
   const size_t smem = ca_smem_bytes(rpc, a.qp, a.q, Q, false);
-  pf->begin("k_ca", st);
-  if (a.op.kind == LRA_OP_FACTORED_CSR) e = launch_cluster(k_ca<Q, TPR, NT, 2>, r, nb, NT, smem, st);
-  else if (a.op.dtype == LRA_F64) e = launch_cluster(k_ca<Q, TPR, NT, 1>, r, nb, NT, smem, st);
-  else e = launch_cluster(k_ca<Q, TPR, NT, 0>, r, nb, NT, smem, st);
-  pf->end(st);
-  return e;
+  if (cs > num_sms() || smem > 227 * 1024 - sizeof(CAShared) - 256 || !a.gscratch || a.y_complex)
+    return cudaErrorInvalidConfiguration;
+  r.cs = cs;
+  r.rpc = rpc;
+  r.grid = 1;
+  if (cs_out) *cs_out = cs;
+  void (*kern)(CAArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? k_ca<Q, TPR, NT, 2>
+                         : (a.op.dtype == LRA_F64 ? k_ca<Q, TPR, NT, 1> : k_ca<Q, TPR, NT, 0>);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const size_t esz = 8;
+  for (int64_t b = 0; b < nb; ++b) {
+    CAArgs rb = r;
+    if (rb.op.kind == LRA_OP_DENSE)
+      rb.op.w = (const char *)rb.op.w + b * rb.w_stride * (rb.op.dtype == LRA_F32 ? 4 : 8);
+    if (rb.Y) rb.Y = (const char *)rb.Y + b * rb.y_stride * esz;
+    if (rb.I0) rb.I0 += b * rb.i0_stride;
+    rb.I += b * a.q;
+    rb.J += b * a.q;
+    if (rb.stats) rb.stats += b;
+    rb.status += b;
+    if (rb.yinfo) rb.yinfo += 4 * b;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cs);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    pf->begin("k_ca_grid", st);
+    e = cudaLaunchKernelEx(&cfg, kern, rb);
+    pf->end(st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t read_ca_counters(unsigned long long *out, bool reset) {

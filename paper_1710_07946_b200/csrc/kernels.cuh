@@ -62,7 +62,12 @@ struct CAArgs {
   lra_ca_stats *stats;         // per problem, may be null
   int32_t *status;             // per problem
   int32_t *yinfo;              // per problem x4: complex stage-2 result (scratch), or null
+  int grid;                    // 1: grid tier (one problem over a cooperative grid)
+  void *gscratch;              // grid tier exchange buffers (ca_grid_scratch_bytes)
 };
+size_t ca_grid_scratch_bytes(int cs);
+// tier chosen for a problem of maxN rows and q columns: 0 none, 1 cluster, 2 grid; cs out
+int ca_tier(int64_t maxN, int q, bool cplx, int *cs_out);
 cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
 cudaError_t read_ca_counters(unsigned long long *out, bool reset);
 

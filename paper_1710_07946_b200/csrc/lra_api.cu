@@ -45,6 +45,8 @@ struct lra_handle_s {
   // scratch arena (grows; reused)
   void *ws;
   size_t ws_bytes;
+  void *gs;                       // grid-tier exchange buffers
+  size_t gs_bytes;
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -200,6 +202,7 @@ lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_
 void lra_handle_destroy(lra_handle h) {
   if (!h) return;
   if (h->ws) cudaFree(h->ws);
+  if (h->gs) cudaFree(h->gs);
   for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
   if (h->streams_ready) {
     for (int i = 0; i < LRA_NSIDE; ++i) {
@@ -303,10 +306,25 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   ca.stats = stats;
   ca.status = status;
   ca.yinfo = y_complex ? yinfo : nullptr;
+  ca.grid = 0;
+  {
+    const size_t gb = ca_grid_scratch_bytes(160);
+    if (h->gs_bytes < gb) {
+      if (h->gs) cudaFree(h->gs);
+      h->gs = nullptr;
+      h->gs_bytes = 0;
+      if (cudaMalloc(&h->gs, gb) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LRA_ENOMEM, "cannot allocate the grid-tier exchange buffers");
+      }
+      h->gs_bytes = gb;
+    }
+    ca.gscratch = h->gs;
+  }
   int cs = 0;
   cudaError_t e = launch_ca(ca, nb, W->m > W->n ? W->m : W->n, st, &cs, &h->prof);
   if (e == cudaErrorInvalidConfiguration)
-    return fail(LRA_EUNSUPPORTED, "block %lld x %lld exceeds the cluster-shared-memory tier",
+    return fail(LRA_EUNSUPPORTED, "block %lld x %lld exceeds the cluster and grid tiers",
                 (long long)(W->m > W->n ? W->m : W->n), (long long)k);
   CK(e);
   h->launches += 1;

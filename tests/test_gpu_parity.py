@@ -217,3 +217,54 @@ def test_argument_errors(P, h):
     Y = torch.empty((8, 256), dtype=torch.float64, device="cuda")
     with pytest.raises(P.LraError):
         P.lra_preprocess(h, W, M, Y)
+
+
+# ------------------------------------------------------------------ config 4 (entry oracle)
+def _factored(P, c4):
+    A_t = torch.from_numpy(np.ascontiguousarray(c4["A"].T)).cuda()      # (p, m): m x p col-major
+    B_t = torch.from_numpy(np.ascontiguousarray(c4["B"].T)).cuda()      # (n, p): p x n col-major
+    rp = torch.from_numpy(c4["row_ptr"]).cuda()
+    col = torch.from_numpy(c4["col"]).cuda()
+    val = torch.from_numpy(c4["val"]).cuda()
+    return P.lra.Factored(A_t, B_t, rp, col, val, c4["m"], c4["n"], c4["p"]), (A_t, B_t, rp, col, val)
+
+
+def _run_config4(P, h, c4, r, k, sweeps, Q, seed=0):
+    from paper_1710_07946_b200 import pipeline
+    op_o = O.FactoredOperand(c4["A"], c4["B"], c4["row_ptr"], c4["col"], c4["val"])
+    I0 = synth.random_rows(seed, c4["m"], k)
+    ca = O.cross_approx(op_o, k, k, sweeps, I0=I0)
+    Uo, Sr, sr, Tr = O.canonical_nucleus(op_o.block(ca.I, ca.J), r)
+    Ao, Bo = O.rank_r_factors(op_o.cols(ca.J), op_o.rows(ca.I), Sr, sr, Tr)
+    ii, jj = synth.sample_pairs(seed, c4["m"], c4["n"], Q)
+    num2_o = O.sampled_residual(op_o, Ao, Bo, ii, jj)
+    den2_o = O.factored_den2(op_o)
+    Wf, keep = _factored(P, c4)
+    bufs = pipeline.CurBuffers(c4["m"], c4["n"], r, k)
+    P.lra_cross_approx(h, Wf, None, torch.from_numpy(I0).cuda(), r, k, k, sweeps, bufs.I, bufs.J, bufs.U,
+                       bufs.A, bufs.B, bufs.stats)
+    P.lra_cur_residual(h, Wf, bufs.A, bufs.B, r, bufs.num2, bufs.den2, nsamples=Q,
+                       si=torch.from_numpy(ii).cuda(), sj=torch.from_numpy(jj).cuda())
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)[0]
+    assert st["status"] == 0
+    assert list(bufs.I.cpu().numpy()) == list(ca.I)
+    assert list(bufs.J.cpu().numpy()) == list(ca.J)
+    assert np.allclose(bufs.U.cpu().numpy().T, Uo, rtol=1e-9, atol=1e-9 * np.abs(Uo).max())
+    assert bufs.num2.item() == pytest.approx(num2_o, rel=1e-6)
+    assert bufs.den2.item() == pytest.approx(den2_o, rel=1e-12)
+
+
+def test_config4_downsized_grid_tier(P, h):
+    """Config-4 recipe at 8192² (p = 16): more rows than one cluster holds, so the C-A runs
+    in the grid tier (cooperative launch, global-memory exchange); entry-oracle operand."""
+    c4 = synth.config4(0, m=8192, n=8192, p=16, dens_ab=0.05, dens_e=1e-3)
+    _run_config4(P, h, c4, 16, 24, 3, 200000)
+
+
+@pytest.mark.slow
+def test_config4_full_size(P, h):
+    """BASELINE config 4 at full size: W = A·B + E, 65536², never materialized; r = 16,
+    k = l = 24, 3 sweeps; residual on 1e6 uniform samples + the exact factored norm."""
+    c4 = synth.config4(0)
+    _run_config4(P, h, c4, 16, 24, 3, 1000000)

@@ -156,3 +156,15 @@ def test_factored_operand_matches_dense():
     assert np.allclose(op.rows(I), Wd[I], atol=1e-14)
     assert np.allclose(op.cols(J), Wd[:, J], atol=1e-14)
     assert lra.factored_den2(op) == pytest.approx(float(np.sum(Wd * Wd)), rel=1e-12)
+
+
+def test_factored_entries_vectorized():
+    """The vectorized entry oracle equals the dense materialization at sampled pairs."""
+    c4 = synth.config4(1, m=300, n=250, p=4, dens_ab=0.3, dens_e=0.02)
+    op = lra.FactoredOperand(c4["A"], c4["B"], c4["row_ptr"], c4["col"], c4["val"])
+    Wd = c4["A"] @ c4["B"]
+    for i in range(op.m):
+        lo, hi = c4["row_ptr"][i], c4["row_ptr"][i + 1]
+        Wd[i, c4["col"][lo:hi]] += c4["val"][lo:hi]
+    ii, jj = synth.sample_pairs(3, 300, 250, 5000)
+    assert np.allclose(op.entries(ii, jj), Wd[ii, jj], atol=1e-14)
