@@ -21,6 +21,7 @@
 // is one launch.  The complex (ARFT) stage-2 maxvol uses a shared-memory row variant.
 #include <cooperative_groups.h>
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -1093,6 +1094,12 @@ static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   CAArgs r = a;
   r.y_complex = 0;
   if (a.y_complex) r.Y = nullptr;
+  static const bool use_old = getenv("LRA_CA_OLD") != nullptr;   // A/B switch (diagnostics)
+  if (!use_old) {                                                // cluster tier, ca_cluster.cu
+    e = launch_ca_cluster(r, nb, maxN, st, cs_out, pf);
+    if (e != cudaErrorInvalidConfiguration) return e;
+    cudaGetLastError();
+  }
   if (pick_cluster(maxN, NT / TPR, a.qp, a.q, Q, false, cs, rpc)) {   // cluster tier
     r.cs = cs;
     r.rpc = rpc;
@@ -1150,12 +1157,18 @@ static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   return cudaSuccess;
 }
 
+// old-kernel counters + cluster-tier counters (ca_cluster.cu), elementwise (one of them is
+// zero for any given run)
 cudaError_t read_ca_counters(unsigned long long *out, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_ca_cyc, sizeof(g_ca_cyc));
   if (e == cudaSuccess && reset) {
     unsigned long long z[16] = {0};
     e = cudaMemcpyToSymbol(g_ca_cyc, z, sizeof(z));
   }
+  unsigned long long c2[16];
+  if (e == cudaSuccess) e = read_cc_counters(c2, reset);
+  if (e == cudaSuccess)
+    for (int i = 0; i < 16; ++i) out[i] += c2[i];
   return e;
 }
 

@@ -70,6 +70,9 @@ size_t ca_grid_scratch_bytes(int cs);
 int ca_tier(int64_t maxN, int q, bool cplx, int *cs_out);
 cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
 cudaError_t read_ca_counters(unsigned long long *out, bool reset);
+// cluster tier of the real C-A (ca_cluster.cu); cudaErrorInvalidConfiguration if it does not fit
+cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
+cudaError_t read_cc_counters(unsigned long long *out, bool reset);
 
 struct NucArgs {
   OpView op;

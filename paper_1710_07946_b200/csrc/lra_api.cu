@@ -32,7 +32,7 @@ static lra_status fail(lra_status s, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(LRA_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));   \
   } while (0)
 
-#define LRA_NSIDE 3
+#define LRA_NSIDE 8
 struct lra_handle_s {
   int device;
   int groups;                     // lra_batch groups (env LRA_BATCH_GROUPS, default 2)
