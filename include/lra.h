@@ -97,9 +97,15 @@ typedef struct {
   double cert_cols;         /* max |C'| at exit of the last horizontal step (<= 1 + tol)     */
 } lra_ca_stats;
 
+/* Precision of the reconstruction A*B inside the full a-posteriori pass.
+   Both run the product on the tcgen05 tensor cores as an exact int8 digit-slice
+   (Ozaki-style) contraction with int32 TMEM accumulators, recombined in fp64:
+   PRECISE uses 6 slices per operand (truncation ~2^-42 of max|A_i| max|B_j| r, enough for
+   rho ~ 1e-8 on fp32 W), FAST 3 slices (~2^-21, fp32-class).  fp64 W in PRECISE mode uses
+   an fp64 FMA kernel instead (fp64-exact to rounding). */
 typedef enum {
-  LRA_RECON_FAST = 0,    /* reserved: tensor-core reconstruction (not in this build)           */
-  LRA_RECON_PRECISE = 1  /* fp64-accurate reconstruction                                       */
+  LRA_RECON_FAST = 0,
+  LRA_RECON_PRECISE = 1
 } lra_recon;
 
 /* Create a handle bound to CUDA device `device`.  nccl_unique_id must be NULL and
@@ -139,7 +145,8 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
    den2 = sum_ij W_ij^2 in fp64 over the full matrix (nsamples == 0), or, when nsamples > 0,
    num2 = (m n / Q) sum_q d_q^2 over the Q given pairs (si[q], sj[q]) and den2
    = the exact ||W||_F^2 (dense: full pass; factored: tr((A^T A)(B B^T)) + 2 sum_E E.(AB) +
-   sum E^2).  num2, den2: device scalars.  prec must be LRA_RECON_PRECISE in this build. */
+   sum E^2).  num2, den2: device scalars.  prec: lra_recon (full pass only; the sampled
+   estimate is always fp64). */
 lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A, const double *B,
                             int64_t r, int32_t prec, int64_t nsamples, const int64_t *si,
                             const int64_t *sj, double *num2, double *den2, void *stream);
@@ -173,6 +180,13 @@ int lra_profile_read(lra_handle h, int cap, const char **names /* host */, doubl
    [8..14] sub-phases of a swap step and of the cluster exchange.
    out16: host array of 16.  Synchronizes the device.  reset != 0 zeroes the counters. */
 lra_status lra_debug_counters(uint64_t *out16 /* host */, int reset);
+
+/* Diagnostics: clock64 cycle counters of the tensor-core residual's warp roles, summed over
+   CTAs: [0] MMA waits for B slices, [1] MMA waits for a free TMEM buffer, [2] MMA issue,
+   [3] producer waits for a free B stage, [4] producer waits for a free A buffer, [5] MMA
+   waits for A, [6] epilogue warp 0 waits for accumulators, [7] epilogue warp 0 work,
+   [8] tiles.  out16: host array of 16.  Synchronizes the device. */
+lra_status lra_debug_counters_residual(uint64_t *out16 /* host */, int reset);
 
 /* Thread-local message for the last non-OK status (never NULL). */
 const char *lra_last_error(void);

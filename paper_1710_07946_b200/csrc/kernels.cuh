@@ -73,6 +73,7 @@ cudaError_t read_ca_counters(unsigned long long *out, bool reset);
 // cluster tier of the real C-A (ca_cluster.cu); cudaErrorInvalidConfiguration if it does not fit
 cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
 cudaError_t read_cc_counters(unsigned long long *out, bool reset);
+cudaError_t read_rtc_counters(unsigned long long *out, bool reset);
 
 struct NucArgs {
   OpView op;
@@ -107,6 +108,13 @@ struct ResArgs {
   const int32_t *status;
 };
 cudaError_t launch_residual(ResArgs a, int64_t nb, double *num2, double *den2, cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_reduce(const double2 *partial, int64_t ntiles, int64_t nb, double *num2, double *den2,
+                          const int32_t *status, cudaStream_t st, int *nlaunch, Prof *pf);
+// tensor-core residual (residual_tc.cu): S digit slices (6 PRECISE, 3 FAST)
+size_t residual_tc_scratch(int64_t m, int64_t n, int r, int S, int64_t nb);
+int64_t residual_tc_partials(int64_t m, int64_t n);
+cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, double *num2, double *den2,
+                               cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,
                            const int64_t *sj, int64_t Q, double2 *partial, int nblk, double *num2,
                            double *den2, cudaStream_t st, int *nlaunch, Prof *pf);

@@ -172,6 +172,28 @@ static SketchArgs make_sketch(const lra_operand *W, const lra_multiplier *M, voi
   return a;
 }
 
+// Reconstruction path of the full residual: fp32 W (or FAST) -> tensor-core
+// Ozaki kernel with S = 6 (PRECISE) / 3 (FAST) int8 digit slices; fp64 W in PRECISE mode ->
+// fp64 SIMT kernel.  LRA_RESID_SIMT=1 forces the SIMT kernel (A/B diagnostics).
+static int resid_slices(int dtype, int prec) {
+  static const bool simt = getenv("LRA_RESID_SIMT") != nullptr;
+  if (prec == LRA_RECON_FAST) return 3;
+  if (dtype == LRA_F32 && !simt) return 6;
+  return 0;
+}
+static size_t resid_scratch(int64_t m, int64_t n, int64_t r, int S, int64_t nb) {
+  const int64_t simt_tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  const int64_t tc_parts = residual_tc_partials(m, n);
+  size_t bytes = (size_t)nb * (simt_tiles > tc_parts ? simt_tiles : tc_parts) * sizeof(double2) + 256;
+  if (S) bytes += residual_tc_scratch(m, n, (int)r, S, nb) + 256;
+  return bytes;
+}
+static int64_t resid_partials(int64_t m, int64_t n) {
+  const int64_t simt_tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  const int64_t tc_parts = residual_tc_partials(m, n);
+  return simt_tiles > tc_parts ? simt_tiles : tc_parts;
+}
+
 extern "C" {
 
 const char *lra_last_error(void) { return g_err.c_str(); }
@@ -253,6 +275,12 @@ int64_t lra_launch_count(lra_handle h) { return h ? h->launches : 0; }
 lra_status lra_debug_counters(uint64_t *out8, int reset) {
   if (!out8 /* 16 entries */) return fail(LRA_EINVAL, "null output");
   CK(read_ca_counters((unsigned long long *)out8, reset != 0));
+  return LRA_OK;
+}
+
+lra_status lra_debug_counters_residual(uint64_t *out16, int reset) {
+  if (!out16) return fail(LRA_EINVAL, "null output");
+  CK(read_rtc_counters((unsigned long long *)out16, reset != 0));
   return LRA_OK;
 }
 
@@ -403,7 +431,7 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   lra_status s;
   if ((s = check_device(h)) != LRA_OK) return s;
   if ((s = check_operand(W)) != LRA_OK) return s;
-  if (prec != LRA_RECON_PRECISE) return fail(LRA_EUNSUPPORTED, "only LRA_RECON_PRECISE is in this build");
+  if (prec != LRA_RECON_PRECISE && prec != LRA_RECON_FAST) return fail(LRA_EINVAL, "bad lra_recon");
   if (!A || !B || !num2 || !den2 || r < 1) return fail(LRA_EINVAL, "null A/B/num2/den2 or r < 1");
   cudaStream_t st = (cudaStream_t)stream;
   if (nsamples > 0) {
@@ -416,8 +444,8 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
     return LRA_OK;
   }
   if (W->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "the full pass needs a dense operand (use nsamples > 0)");
-  const int64_t tiles = ((W->m + 127) / 128) * ((W->n + 127) / 128);
-  if ((s = ws_reserve(h, (size_t)tiles * sizeof(double2) + 256)) != LRA_OK) return s;
+  const int S = resid_slices(W->dtype, prec);
+  if ((s = ws_reserve(h, resid_scratch(W->m, W->n, r, S, 1))) != LRA_OK) return s;
   ResArgs a{};
   a.dtype = W->dtype;
   a.m = W->m;
@@ -430,7 +458,12 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   a.partial = (double2 *)h->ws;
   a.status = nullptr;
   int nl = 0;
-  CK(launch_residual(a, 1, num2, den2, st, &nl, &h->prof));
+  if (S) {
+    char *tcs = (char *)h->ws + (((size_t)resid_partials(W->m, W->n) * sizeof(double2) + 255) & ~(size_t)255);
+    CK(launch_residual_tc(a, 1, S, tcs, num2, den2, st, &nl, &h->prof));
+  } else {
+    CK(launch_residual(a, 1, num2, den2, st, &nl, &h->prof));
+  }
   h->launches += nl;
   return LRA_OK;
 }
@@ -450,12 +483,13 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   if (M0->lbar != k) return fail(LRA_EINVAL, "v1 requires lbar == k (reading C9)");
   if (m_stride != 0 && M0->kind != LRA_MUL_SPARSE_PM1)
     return fail(LRA_EINVAL, "per-block multipliers (m_stride != 0) are supported for SPARSE_PM1 only");
-  if (prec != LRA_RECON_PRECISE) return fail(LRA_EUNSUPPORTED, "only LRA_RECON_PRECISE is in this build");
+  if (prec != LRA_RECON_PRECISE && prec != LRA_RECON_FAST) return fail(LRA_EINVAL, "bad lra_recon");
   if (!I || !J || !num2 || !den2) return fail(LRA_EINVAL, "null output");
   const int64_t m = W0->m, n = W0->n;
   const bool cplx = M0->kind == LRA_MUL_ARFT;
   const size_t esz = cplx ? 16 : 8;
-  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  const int64_t tiles = resid_partials(m, n);
+  const int S = resid_slices(W0->dtype, prec);
   Carve probe{nullptr, 0};
   probe.take<int32_t>(nb);
   probe.take<char>((size_t)nb * m * k * esz);
@@ -465,6 +499,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   probe.take<double>((size_t)nb * r * n);
   probe.take<double2>((size_t)nb * tiles);
   probe.take<int32_t>((size_t)nb * 4);
+  probe.take<char>(S ? residual_tc_scratch(m, n, (int)r, S, nb) : 0);
   if ((s = ws_reserve(h, probe.off + 256)) != LRA_OK) return s;
   Carve cv{(char *)h->ws, 0};
   int32_t *status = cv.take<int32_t>(nb);
@@ -475,6 +510,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   double *B = cv.take<double>((size_t)nb * r * n);
   double2 *part = cv.take<double2>((size_t)nb * tiles);
   int32_t *yinfo = cv.take<int32_t>((size_t)nb * 4);
+  char *tcs = S ? cv.take<char>(residual_tc_scratch(m, n, (int)r, S, nb)) : nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(status, 0, sizeof(int32_t) * nb, st));
   // Blocks are processed in groups on the handle's side streams (fork/join on `stream` with
@@ -523,7 +559,13 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
     ra.partial = part + b0 * tiles;
     ra.status = status + b0;
     int nl = 0;
-    CK(launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof));
+    if (S) {   // each group uses its own slice of the tensor-core scratch
+      char *g_tcs = tcs + (residual_tc_scratch(m, n, (int)r, S, nb) - 1024) / nb * b0;
+      g_tcs = (char *)(((uintptr_t)g_tcs + 255) & ~(uintptr_t)255);
+      CK(launch_residual_tc(ra, gn, S, g_tcs, num2 + b0, den2 + b0, gs, &nl, &h->prof));
+    } else {
+      CK(launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof));
+    }
     h->launches += nl;
   }
   for (int i = 0; i < LRA_NSIDE; ++i) {

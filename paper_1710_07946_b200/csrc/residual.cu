@@ -159,6 +159,15 @@ __global__ void __launch_bounds__(256) k_reduce(const double2 *partial, int64_t 
   }
 }
 
+cudaError_t launch_reduce(const double2 *partial, int64_t ntiles, int64_t nb, double *num2, double *den2,
+                          const int32_t *status, cudaStream_t st, int *nlaunch, Prof *pf) {
+  pf->begin("k_reduce", st);
+  k_reduce<<<(unsigned)nb, 256, 0, st>>>(partial, ntiles, num2, den2, 1.0, status);
+  pf->end(st);
+  *nlaunch += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_residual(ResArgs a, int64_t nb, double *num2, double *den2, cudaStream_t st, int *nlaunch, Prof *pf) {
   a.tiles_m = (a.m + RS_T - 1) / RS_T;
   a.tiles_n = (a.n + RS_T - 1) / RS_T;

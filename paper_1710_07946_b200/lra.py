@@ -81,6 +81,8 @@ def _load():
     lib.lra_profile_read.restype = C.c_int
     lib.lra_debug_counters.argtypes = [P(C.c_uint64), C.c_int]
     lib.lra_debug_counters.restype = C.c_int
+    lib.lra_debug_counters_residual.argtypes = [P(C.c_uint64), C.c_int]
+    lib.lra_debug_counters_residual.restype = C.c_int
     for f in ("lra_handle_create", "lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
         getattr(lib, f).restype = C.c_int
     return lib
@@ -98,7 +100,7 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read", "lra_debug_counters"]
+            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual"]
 
 
 def debug_counters(reset=True):
@@ -106,6 +108,14 @@ def debug_counters(reset=True):
     _check(lib().lra_debug_counters(out, int(reset)))
     names = ["load", "cold_lu", "warm_gather", "gauss_jordan", "product", "swap_loop", "kernel", "pivot_steps",
              "sw_ctamax", "sw_ctaidx", "sw_pub", "x_barrier", "x_triples", "x_prow", "sw_update", "-"]
+    return dict(zip(names, [int(x) for x in out]))
+
+
+def debug_counters_residual(reset=True):
+    out = (C.c_uint64 * 16)()
+    _check(lib().lra_debug_counters_residual(out, int(reset)))
+    names = ["mma_wait_b", "mma_wait_tmem", "mma_issue", "prod_wait_b", "prod_wait_a", "mma_wait_a",
+             "epi_wait_tmem", "epi_work", "tiles", "epi_ldtm", "epi_wait_w"]
     return dict(zip(names, [int(x) for x in out]))
 
 

@@ -268,3 +268,53 @@ def test_config4_full_size(P, h):
     k = l = 24, 3 sweeps; residual on 1e6 uniform samples + the exact factored norm."""
     c4 = synth.config4(0)
     _run_config4(P, h, c4, 16, 24, 3, 1000000)
+
+
+# ------------------------------------------------------------------ tensor-core residual (a5)
+def _residual_gpu(P, h, W, A, B, r, prec):
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    Bt = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    num2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    den2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.lra_cur_residual(h, _dense(P, W), At, Bt, r, num2, den2, prec=prec)
+    torch.cuda.synchronize()
+    return num2.item(), den2.item()
+
+
+def test_residual_tc_config2_oracle_factors(P, h):
+    """a5 in isolation on BASELINE config 2 (fp32 4096², r = 32, rho ~ 7e-7): the tensor-core
+    int8 digit-slice product (PRECISE, 6 slices) reproduces the oracle's fp64 rho to 1e-6
+    relative given the oracle's own A, B (so the only difference is the product arithmetic)."""
+    W = synth.config2(0)
+    M = synth.multiplier_abridged(0, 4096, 4, 48, "arht")
+    ora = O.cur_pipeline(W, M, 32, 48, 48, 3)
+    num2, den2 = _residual_gpu(P, h, W, ora.A, ora.B, 32, P.lra.LRA_RECON_PRECISE)
+    assert den2 == pytest.approx(ora.den2, rel=1e-13)
+    assert abs(np.sqrt(num2 / den2) / ora.rho - 1) <= 1e-6, (np.sqrt(num2 / den2), ora.rho)
+
+
+@pytest.mark.parametrize("m,n,r", [(1000, 776, 9), (333, 520, 7), (130, 96, 3), (700, 300, 40), (257, 4099, 32)])
+def test_residual_tc_ragged(P, h, m, n, r):
+    """Ragged edges (partial 128-row blocks, partial 32-column tiles, r < 32 and r > 32 = two
+    K blocks): fp32 W, PRECISE; compared with the oracle's fp64 residual on the same A, B."""
+    g = np.random.default_rng(m * 7 + n)
+    A = g.standard_normal((m, r))
+    B = g.standard_normal((r, n))
+    W = (A @ B + 1e-5 * g.standard_normal((m, n))).astype(np.float32)
+    num_o, den_o = O.cur_residual(W, A, B)
+    num2, den2 = _residual_gpu(P, h, np.asfortranarray(W), A, B, r, P.lra.LRA_RECON_PRECISE)
+    assert den2 == pytest.approx(den_o, rel=1e-13)
+    assert num2 == pytest.approx(num_o, rel=1e-6)
+
+
+def test_residual_tc_fast_mode(P, h):
+    """FAST (3 slices, ~2^-21): fine where rho is far above fp32 level (config-5-like noise)."""
+    g = np.random.default_rng(5)
+    m, n, r = 2048, 1024, 64
+    A = g.standard_normal((m, r)) / 8
+    B = g.standard_normal((r, n)) / 8
+    W = (A @ B + 0.1 * g.standard_normal((m, n))).astype(np.float32)
+    num_o, den_o = O.cur_residual(W, A, B)
+    num2, den2 = _residual_gpu(P, h, np.asfortranarray(W), A, B, r, P.lra.LRA_RECON_FAST)
+    assert num2 == pytest.approx(num_o, rel=1e-4)
+    assert den2 == pytest.approx(den_o, rel=1e-13)
