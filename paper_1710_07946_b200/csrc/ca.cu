@@ -1172,6 +1172,21 @@ cudaError_t read_ca_counters(unsigned long long *out, bool reset) {
   return e;
 }
 
+bool ca_needs_global(int64_t maxN, int q) {
+  static const bool force = getenv("LRA_CA_FORCE_GLOBAL") != nullptr;   // diagnostics / tests
+  if (force || q > LRA_QMAX) return true;
+  // cluster tier (ca_cluster.cu): 16 CTAs x 512/TPR rows (TPR = 1 for q <= 24, else 2)
+  const int64_t rpc_cl = q <= 24 ? 512 : 256;
+  if (q <= 48 && maxN <= 16 * rpc_cl) return false;
+  // grid tier (ca.cu): one CTA per SM, NT/TPR = 256 rows each (TPR = 2 for q > 24)
+  const int64_t rpc_g = q <= 24 ? 512 : 256;
+  if (maxN <= (int64_t)num_sms() * rpc_g &&
+      ca_smem_bytes((int)rpc_g, q | 1, q, q <= 8 ? 8 : (q <= 16 ? 16 : (q <= 24 ? 24 : (q <= 32 ? 32 : (q <= 48 ? 48 : 64)))),
+                    false) <= 227 * 1024 - sizeof(CAShared) - 256)
+    return false;
+  return true;
+}
+
 cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
   // (Q, threads per row, CTA threads): W = Q/TPR doubles of the row per lane
   if (a.q <= 8) return launch_ca_t<8, 1, 512>(a, nb, maxN, st, cs_out, pf);

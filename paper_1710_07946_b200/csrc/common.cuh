@@ -7,7 +7,8 @@
 #include "../../include/lra.h"
 
 #define LRA_NT 512          // threads of the maxvol / C-A CTAs
-#define LRA_QMAX 64         // largest k = l handled by the cluster tiers
+#define LRA_QMAX 64         // largest k = l handled by the on-chip (cluster / grid) tiers
+#define LRA_QMAX_ALL 128    // largest k = l handled at all (global-memory tier)
 
 // ----------------------------------------------------------------------------- complex
 struct cplx {

@@ -47,6 +47,8 @@ struct lra_handle_s {
   size_t ws_bytes;
   void *gs;                       // grid-tier exchange buffers
   size_t gs_bytes;
+  void *gm;                       // global-memory C-A tier (block + C-matrix)
+  size_t gm_bytes;
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -225,6 +227,7 @@ void lra_handle_destroy(lra_handle h) {
   if (!h) return;
   if (h->ws) cudaFree(h->ws);
   if (h->gs) cudaFree(h->gs);
+  if (h->gm) cudaFree(h->gm);
   for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
   if (h->streams_ready) {
     for (int i = 0; i < LRA_NSIDE; ++i) {
@@ -302,7 +305,7 @@ static lra_status check_ca_shape(const lra_operand *W, int64_t r, int64_t k, int
   if (k != l) return fail(LRA_EINVAL, "v1 requires k == l (reading C9)");
   if (r < 1 || r > k) return fail(LRA_EINVAL, "need 0 < r <= k");
   if (k > W->m || l > W->n) return fail(LRA_EINVAL, "need k <= m and l <= n");
-  if (k > LRA_QMAX) return fail(LRA_EUNSUPPORTED, "k > %d is outside this build's maxvol tiers", LRA_QMAX);
+  if (k > LRA_QMAX_ALL) return fail(LRA_EUNSUPPORTED, "k > %d is outside this build's maxvol tiers", LRA_QMAX_ALL);
   if (sweeps < 1) return fail(LRA_EINVAL, "sweeps >= 1");
   return LRA_OK;
 }
@@ -350,12 +353,30 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
     ca.gscratch = h->gs;
   }
   int cs = 0;
-  cudaError_t e = launch_ca(ca, nb, W->m > W->n ? W->m : W->n, st, &cs, &h->prof);
+  const int64_t maxN = W->m > W->n ? W->m : W->n;
+  cudaError_t e;
+  if (ca_needs_global(maxN, (int)k)) {
+    if (y_complex) return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
+    const size_t gb = ca_global_scratch_bytes(maxN, (int)k);
+    if (h->gm_bytes < gb) {
+      if (h->gm) cudaFree(h->gm);
+      h->gm = nullptr;
+      h->gm_bytes = 0;
+      if (cudaMalloc(&h->gm, gb) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the global-memory C-A tier", gb);
+      }
+      h->gm_bytes = gb;
+    }
+    e = launch_ca_global(ca, nb, maxN, h->gm, st, &h->prof);
+    if (e == cudaSuccess) h->launches += nb;
+  } else {
+    e = launch_ca(ca, nb, maxN, st, &cs, &h->prof);
+    if (e == cudaSuccess) h->launches += 1;
+  }
   if (e == cudaErrorInvalidConfiguration)
-    return fail(LRA_EUNSUPPORTED, "block %lld x %lld exceeds the cluster and grid tiers",
-                (long long)(W->m > W->n ? W->m : W->n), (long long)k);
+    return fail(LRA_EUNSUPPORTED, "block %lld x %lld exceeds the C-A tiers", (long long)maxN, (long long)k);
   CK(e);
-  h->launches += 1;
   NucArgs na{};
   na.op = ca.op;
   na.w_stride = w_stride;

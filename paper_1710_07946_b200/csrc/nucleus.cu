@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   // cos(angle) between two columns exceeds 4·k·eps (the fp64 dot products of already
   // orthogonal columns carry relative errors ~k·eps, so a tighter test never stops).
   double *nrm = sig;                   // cached squared column norms (L)
-  __shared__ unsigned char s_pair[63 * 32 * 2];   // round-robin schedule (L <= 64)
+  __shared__ unsigned char s_pair[127 * 64 * 2];  // round-robin schedule (L <= 128)
   for (int e = tid; e < (L - 1) * (L / 2); e += NT) {
     int p, qq;
     rr_pair(L, e / (L / 2), e % (L / 2), p, qq);
@@ -78,10 +78,10 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
       for (int pi = warp; pi < L / 2; pi += NW) {
         const int p = s_pair[2 * (round * (L / 2) + pi)], qq = s_pair[2 * (round * (L / 2) + pi) + 1];
         double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
-        double xv[2], yv[2];
+        double xv[4], yv[4];
         double ga = 0.0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
           const int i = lane + 32 * u;
           xv[u] = i < k ? gp[i] : 0.0;
           yv[u] = i < k ? gq[i] : 0.0;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
           const double t = copysign(__drcp_rn(fabs(zeta) + h), zeta);
           const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < 4; ++u) {
             const int i = lane + 32 * u;
             if (i < k) {
               gp[i] = cs * xv[u] - sn * yv[u];
@@ -104,8 +104,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
             }
           }
           double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < 4; ++u) {
             const int i = lane + 32 * u;
             if (i < L) {
               const double x = vp[i], y = vq[i];
@@ -178,7 +177,7 @@ size_t nucleus_smem(int k, int l) {
 
 // A = W[:,J] * TS.  grid (ceil(m/64), nb), 256 threads = 64 rows x 4 chunks of 16 outputs
 __global__ void __launch_bounds__(256) k_factor_A(FacArgs a) {
-  __shared__ double ts[LRA_QMAX * LRA_QMAX];
+  extern __shared__ double ts[];          // l x r
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
@@ -212,7 +211,7 @@ __global__ void __launch_bounds__(256) k_factor_A(FacArgs a) {
 
 // B = Sr^T * W[I,:].  grid (ceil(n/64), nb), 256 threads = 64 columns x 4 chunks
 __global__ void __launch_bounds__(256) k_factor_B(FacArgs a) {
-  __shared__ double sr[LRA_QMAX * LRA_QMAX];
+  extern __shared__ double sr[];          // k x r
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
@@ -250,18 +249,22 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   if (e != cudaSuccess) return e;
   pf->begin("k_nucleus", st);
   const int L = (na.l + 1) & ~1;
-  const int nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
+  int nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
+  if (nt > 1024) nt = 1024;
   k_nucleus<<<(unsigned)nb, nt, smem, st>>>(na);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   dim3 gA((unsigned)((fa.op.m + 63) / 64), (unsigned)nb);
+  const size_t sA = (size_t)fa.l * fa.r * 8, sB = (size_t)fa.k * fa.r * 8;
+  if ((e = cudaFuncSetAttribute(k_factor_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sA)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k_factor_B, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sB)) != cudaSuccess) return e;
   pf->begin("k_factor_A", st);
-  k_factor_A<<<gA, 256, 0, st>>>(fa);
+  k_factor_A<<<gA, 256, sA, st>>>(fa);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   dim3 gB((unsigned)((fa.op.n + 63) / 64), (unsigned)nb);
   pf->begin("k_factor_B", st);
-  k_factor_B<<<gB, 256, 0, st>>>(fa);
+  k_factor_B<<<gB, 256, sB, st>>>(fa);
   pf->end(st);
   *nlaunch += 3;
   return cudaGetLastError();

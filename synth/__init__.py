@@ -202,3 +202,41 @@ def sample_pairs(seed: int, m: int, n: int, q: int):
     """q i.i.d. uniform (i, j) pairs for the sampled a-posteriori check."""
     g = rng(seed, S_SAMPLES)
     return g.integers(0, m, size=q).astype(np.int64), g.integers(0, n, size=q).astype(np.int64)
+
+
+# ------------------------------------------------------------ config 5 (device generator)
+def config5_factors(seed: int, m: int, n: int, p: int = 64):
+    """U (m×p), V (n×p) with orthonormal columns: Q factors (diag R > 0, reading C20) of
+    i.i.d. N(0,1) matrices from Philox streams (seed, 50) / (seed, 51); fp64, host."""
+    U = _q_factor(_normal_colmajor(rng(seed, 50), m, p))
+    V = _q_factor(_normal_colmajor(rng(seed, 51), n, p))
+    return U, V
+
+
+def config5_torch(seed: int, m: int, n: int, row0: int = 0, rows: int = None, device="cuda",
+                  noise_std: float = 1e-4, factors=None, block: int = 1024):
+    """Row shard [row0, row0+rows) of W = U·diag(σ)·Vᵀ + N (BASELINE config 5; σ_i =
+    10^(-3(i-1)/63), N i.i.d. N(0, 1e-8), i.e. std 1e-4 — reading C15), generated on
+    ``device`` as a (n, rows) fp32 tensor = the column-major m_local×n shard.  The noise of
+    every 1024-row block comes from its own seeded torch generator, so a shard's bits do not
+    depend on how the rows are split over ranks."""
+    import torch
+    rows = m - row0 if rows is None else rows
+    U, V = factors if factors is not None else config5_factors(seed, m, n)
+    sig = config5_sigma(U.shape[1])
+    Us = torch.from_numpy(np.ascontiguousarray((U[row0:row0 + rows] * sig[None, :]).T)).to(device, torch.float32)
+    Vt = torch.from_numpy(np.ascontiguousarray(V)).to(device, torch.float32)
+    out = torch.empty((n, rows), dtype=torch.float32, device=device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        torch.matmul(Vt, Us, out=out)                       # (n, rows) = V · (U_shard σ)ᵀ
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    b0 = row0 // block
+    for b in range(b0, (row0 + rows + block - 1) // block):
+        lo, hi = max(b * block, row0), min((b + 1) * block, row0 + rows)
+        g = torch.Generator(device=device).manual_seed(int(seed) * 1000003 + b)
+        z = torch.randn((n, block), generator=g, device=device, dtype=torch.float32)
+        out[:, lo - row0:hi - row0] += noise_std * z[:, lo - b * block:hi - b * block]
+    return out

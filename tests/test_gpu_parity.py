@@ -318,3 +318,57 @@ def test_residual_tc_fast_mode(P, h):
     num2, den2 = _residual_gpu(P, h, np.asfortranarray(W), A, B, r, P.lra.LRA_RECON_FAST)
     assert num2 == pytest.approx(num_o, rel=1e-4)
     assert den2 == pytest.approx(den_o, rel=1e-13)
+
+
+# ------------------------------------------------------------ global-memory C-A tier
+def test_global_tier_q96_vs_oracle(P, h):
+    """q = 96 > 64 selects the global-memory tier (cooperative grid, C-matrix in L2):
+    pivots bit-exact vs the oracle, certificates <= 1 + 1e-12."""
+    m, n, r, k = 3000, 2600, 64, 96
+    W = np.asfortranarray(synth.factor_gaussian(21, m, n, r, 1e-10).astype(np.float32))
+    M = synth.multiplier_abridged(5, n, 3, k, "arht")
+    _check_pipeline(P, h, W, M, r, k, 3, rho_tol_rel=1e-4)
+
+
+def _run_forced_global(script):
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, LRA_CA_FORCE_GLOBAL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", script], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    return p.stdout
+
+
+def test_global_tier_forced_matches_oracle_config2():
+    """The global-memory tier forced onto BASELINE config 2 (fp32 4096², k = 48, ARHT d=4,
+    3 sweeps) in a subprocess: pivots and swap counts equal the oracle's."""
+    out = _run_forced_global(
+        "import json, numpy as np, torch, synth\n"
+        "from paper_1710_07946_b200 import Handle, lra, pipeline\n"
+        "W = synth.config2(0); M = synth.multiplier_abridged(0, 4096, 4, 48, 'arht')\n"
+        "h = Handle(0); b = pipeline.cur(h, lra.Dense(lra.to_colmajor(W)), lra.Multiplier(M), 32, 48, 3)\n"
+        "torch.cuda.synchronize(); st = lra.stats_to_numpy(b.stats)[0]\n"
+        "print(json.dumps({'I': b.I.cpu().tolist(), 'J': b.J.cpu().tolist(), 'swaps': int(st['swaps']),"
+        " 'status': int(st['status']), 'rho': float(np.sqrt(b.num2.item() / b.den2.item()))}))\n")
+    import json
+    g = json.loads(out.strip().splitlines()[-1])
+    W = synth.config2(0)
+    ora = O.cur_pipeline(W, synth.multiplier_abridged(0, 4096, 4, 48, "arht"), 32, 48, 48, 3)
+    assert g["status"] == 0
+    assert g["I"] == list(ora.I) and g["J"] == list(ora.J)
+    assert g["swaps"] == ora.ca.swaps
+    assert abs(g["rho"] / ora.rho - 1) <= 1e-4
+
+
+def test_config5_recipe_downsized(P, h):
+    """BASELINE config 5 recipe (W = U diag(σ) Vᵀ + N, σ_i = 10^(-3(i-1)/63), noise std 1e-4,
+    r = 64, k = l = 96, ARHT d = 5, 3 sweeps) at 16384² on one GPU, generated on device and
+    copied to the oracle: pivots bit-exact, ρ within 1e-4 (ρ ≈ 0.98: noise-dominated)."""
+    m = n = 16384
+    Wt = synth.config5_torch(0, m, n)
+    W = Wt.cpu().numpy().T
+    M = synth.multiplier_abridged(0, n, 5, 96, "arht")
+    rho, ora = _check_pipeline(P, h, np.asfortranarray(W), M, 64, 96, 3, rho_tol_rel=1e-4)
+    assert 0.5 < rho < 1.0
