@@ -59,6 +59,10 @@ typedef struct {
   int64_t p;
   const int64_t *e_rowptr, *e_col;
   const double *e_val;
+  /* Row sharding (multi-GPU): this rank holds rows [row0, row0 + m) of an
+     m_global x n matrix (DENSE only).  m_global = 0: not sharded.  Requires a handle created
+     with an NCCL communicator; every rank calls the entry points in the same order. */
+  int64_t row0, m_global;
 } lra_operand;
 
 /* Realized randomized multiplier M (n x lbar). */
@@ -108,11 +112,14 @@ typedef enum {
   LRA_RECON_PRECISE = 1
 } lra_recon;
 
-/* Create a handle bound to CUDA device `device`.  nccl_unique_id must be NULL and
-   nranks == 1 in this build (multi-GPU runs deal independent problems to ranks, DESIGN.md
-   §9); other values return LRA_EUNSUPPORTED. */
+/* Create a handle bound to CUDA device `device`.  nccl_unique_id (host, 128 bytes from
+   lra_nccl_unique_id on one rank, distributed by the caller) creates an NCCL communicator of
+   nranks ranks (this one = rank) used by the row-sharded path; NULL (with nranks == 1) for
+   single-GPU use.  NCCL is loaded at run time (libnccl.so.2); LRA_ENCCL if it cannot be. */
 lra_status lra_handle_create(lra_handle *h /* host */, int device, const void *nccl_unique_id,
                              int nranks, int rank);
+/* Write a fresh NCCL unique id (128 bytes) to out (host). */
+lra_status lra_nccl_unique_id(void *out /* host, 128 bytes */);
 void lra_handle_destroy(lra_handle h);
 
 /* Stage 1 of Alg 10.2: Y = W * M, an m x lbar fp64 column-major matrix
@@ -124,7 +131,11 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W /* host struct */,
                           const lra_multiplier *M /* host struct */, void *Y, int64_t ldy,
                           void *stream);
 
-/* Stages 2-3 of Alg 10.2 with C-A at stage 3 (Remark rerfnhmt), then Alg 3.1:
+/* Row-sharded operands (W.m_global > 0): the sketch Y is this rank's m x lbar part; every C-A
+   block (Y, W[I,:]^T, W[:,J], W[I,J]) is assembled on every rank by an exact NCCL sum of the
+   owners' rows and the maxvol runs replicated, so I, J, U, B are identical on every rank and
+   equal to the single-GPU result; A holds this rank's rows.  ARFT sketches are not sharded.
+   Stages 2-3 of Alg 10.2 with C-A at stage 3 (Remark rerfnhmt), then Alg 3.1:
      I <- maxvol(Y) (cold)  or  I <- I0 (if Y == NULL);
      for loop < sweeps:  J <- maxvol(W[I,:]^T, warm from J after loop 1)
                          I <- maxvol(W[:,J],  warm from I);  stop when a later loop swaps nothing;
@@ -146,7 +157,8 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
    num2 = (m n / Q) sum_q d_q^2 over the Q given pairs (si[q], sj[q]) and den2
    = the exact ||W||_F^2 (dense: full pass; factored: tr((A^T A)(B B^T)) + 2 sum_E E.(AB) +
    sum E^2).  num2, den2: device scalars.  prec: lra_recon (full pass only; the sampled
-   estimate is always fp64). */
+   estimate is always fp64).  Row-sharded W: local rows with the local A, then an NCCL sum
+   of num2 and den2 (the sampled estimate is not sharded). */
 lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A, const double *B,
                             int64_t r, int32_t prec, int64_t nsamples, const int64_t *si,
                             const int64_t *sj, double *num2, double *den2, void *stream);

@@ -8,6 +8,6 @@ is no CPU fallback anywhere in the product path.
 """
 from . import lra  # noqa: F401
 from .lra import (Dense, Factored, Handle, LraError, Multiplier, lra_batch, lra_cross_approx,  # noqa: F401
-                  lra_cur_residual, lra_handle_create, lra_preprocess)
+                  lra_cur_residual, lra_handle_create, lra_preprocess, nccl_unique_id)
 
 lra.lib()   # load now: missing/stale builds surface at import time

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
   int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0, sw_h = 0;
   double cert_r = 0.0, cert_c = 0.0;
   const bool yreal = a.Y != nullptr && !a.y_complex;
-  if (!yreal) {
+  if (!yreal || a.y_warm) {
     if (threadIdx.x < q) sh.S[0][threadIdx.x] = a.I0[b * a.i0_stride + threadIdx.x];
     if (a.yinfo) {
       status = a.yinfo[4 * b + 0];
@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
     const int kind = step == 0 ? 0 : ((step & 1) ? 1 : 2);   // 0 = Y, 1 = h, 2 = v
     const int64_t N = kind == 1 ? op.n : op.m;
     long long *S = kind == 1 ? sh.S[1] : sh.S[0];
-    const bool cold = step <= 1;
+    const bool fresh = step <= 1;                     // G^{-1} by Gauss-Jordan (no carried inverse)
+    const bool cold = fresh && !(step == 0 && a.y_warm);   // LUP cold start
     // the inverse is carried only into a following warm step
     const bool carry = step >= 1 && step < last;
     const int nloc = (int)max((int64_t)0, min((int64_t)rpc, N - r0));
@@ -499,7 +500,13 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
       CC_T1(1);
       if (!ok) { status = LRA_ESINGULAR; break; }
       lu += q;
+    } else if (has) {
+      for (int s2 = 0; s2 < q; ++s2)
+        if (S[s2] == grow) myslot = s2;
+    }
+    if (fresh) {
       // ---- G = B[S,:] (original rows, owners' shared memory) -> G^{-1} in part 0
+      if (!cold && k.cs > 1) cluster_sync_all();        // every CTA's block rows are loaded
       {
         CC_T0();
         ib = 0;
@@ -509,9 +516,6 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
       if (!ok) { status = LRA_ESINGULAR; break; }
     } else {
       CC_T0();
-      if (has)
-        for (int s2 = 0; s2 < q; ++s2)
-          if (S[s2] == grow) myslot = s2;
       // carried X0 = (G_prev^{-1})^T, one Newton step against the freshly gathered G
       const int cur = ib, pa = (ib + 1) % 3, pb = (ib + 2) % 3;
       double *Xc = Xp + cur * Q * Q, *Xa = Xp + pa * Q * Q, *Xb = Xp + pb * Q * Q;
@@ -645,7 +649,10 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
     if (!ok) { status = LRA_ESINGULAR; break; }
     swaps += nsw;
     caps += cap_hit;
-    if (kind == 0) sk_swaps = nsw;
+    if (kind == 0) {
+      sk_swaps = nsw;
+      cert_r = cert;
+    }
     if (kind == 1) { cert_c = cert; sw_h = nsw; }
     if (kind == 2) {
       cert_r = cert;

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
   int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0, sw_h = 0;
   double cert_r = 0.0, cert_c = 0.0;
   const bool yreal = a.Y != nullptr && !a.y_complex;
-  if (!yreal) {
+  if (!yreal || a.y_warm) {
     if (tid < q) sh.S[0][tid] = a.I0[tid];
     if (a.yinfo) {
       status = a.yinfo[0];
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
     const int kind = step == 0 ? 0 : ((step & 1) ? 1 : 2);   // 0 = Y, 1 = h, 2 = v
     const int64_t N = kind == 1 ? op.n : op.m;
     long long *S = kind == 1 ? sh.S[1] : sh.S[0];
-    const bool cold = step <= 1;
+    const bool cold = step <= 1 && !(step == 0 && a.y_warm);
     const int64_t rpc = (N + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * rpc, r1 = min(N, r0 + rpc);
     const int iters = (int)((rpc + RPP - 1) / RPP);
@@ -554,7 +554,10 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
     if (!ok) { status = LRA_ESINGULAR; break; }
     swaps += nsw;
     caps += cap_hit;
-    if (kind == 0) sk_swaps = nsw;
+    if (kind == 0) {
+      sk_swaps = nsw;
+      cert_r = cert;
+    }
     if (kind == 1) { cert_c = cert; sw_h = nsw; }
     if (kind == 2) {
       cert_r = cert;

@@ -63,6 +63,7 @@ struct CAArgs {
   int32_t *status;             // per problem
   int32_t *yinfo;              // per problem x4: complex stage-2 result (scratch), or null
   int grid;                    // 1: grid tier (one problem over a cooperative grid)
+  int y_warm;                  // 1: the maxvol on Y starts from the slots I0 (no LUP)
   void *gscratch;              // grid tier exchange buffers (ca_grid_scratch_bytes)
 };
 size_t ca_grid_scratch_bytes(int cs);
@@ -88,6 +89,7 @@ struct NucArgs {
   double *U;              // l x k per problem (stride l*k), may be null
   double *TS, *Sr;        // scratch: l x r and k x r per problem
   int32_t *status;        // per problem: already LRA_ESINGULAR -> skip
+  const double *Gd;       // optional dense G = W[I,J] (k x l col-major) instead of gathering
 };
 struct FacArgs {
   OpView op;
@@ -98,7 +100,17 @@ struct FacArgs {
   double *A, *B;            // A: m x r (lda = m) per problem; B: r x n (ld r) per problem
   int64_t a_stride, b_stride;
   const int32_t *status;
+  const double *Rt;         // optional dense R^T = W[I,:]^T (n x k col-major, ld n) for B
 };
+// row-sharded operands (shard.cu): owner-scattered blocks, assembled by an NCCL sum
+cudaError_t launch_scatter_rows(const double *src, int64_t ld, int64_t m_local, int q, int64_t row0,
+                                int64_t m_global, double *dst, cudaStream_t st);
+cudaError_t launch_scatter_wcols(const OpView &op, const int64_t *J, int q, int64_t row0, int64_t m_global,
+                                 double *dst, cudaStream_t st);
+cudaError_t launch_scatter_wrows(const OpView &op, const int64_t *I, int q, int64_t row0, double *dst,
+                                 cudaStream_t st);
+cudaError_t launch_scatter_g(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, int64_t row0,
+                             double *dst, cudaStream_t st);
 cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf);
 
 struct ResArgs {

@@ -8,11 +8,40 @@
 
 #include <cstdarg>
 
+#include <dlfcn.h>
+#include <nccl.h>      // types only: the functions are resolved at run time (dlopen)
+
+#include <vector>
+
 #include "kernels.cuh"
 
-
-
 using namespace lra;
+
+// ---- NCCL, loaded on first use (no link-time dependency for single-GPU use)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  const char *(*GetErrorString)(ncclResult_t);
+};
+static NcclApi &nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);   // torch's copy if loaded
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(lib, "ncclAllReduce");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+  });
+  return api;
+}
 
 static thread_local std::string g_err = "no error";
 
@@ -32,6 +61,12 @@ static lra_status fail(lra_status s, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(LRA_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));   \
   } while (0)
 
+#define NK(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) return fail(LRA_ENCCL, "%s: %s", #call, nccl().GetErrorString(r_));  \
+  } while (0)
+
 #define LRA_NSIDE 8
 struct lra_handle_s {
   int device;
@@ -40,6 +75,7 @@ struct lra_handle_s {
   cudaEvent_t fork, join[LRA_NSIDE];
   bool streams_ready;
   int nranks, rank;
+  ncclComm_t comm;                // row-sharded path (nullptr: single GPU)
   int64_t launches;
   Prof prof;
   // scratch arena (grows; reused)
@@ -49,6 +85,8 @@ struct lra_handle_s {
   size_t gs_bytes;
   void *gm;                       // global-memory C-A tier (block + C-matrix)
   size_t gm_bytes;
+  void *sh;                       // row-sharded path: assembled blocks
+  size_t sh_bytes;
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -109,6 +147,10 @@ static OpView make_view(const lra_operand *W) {
 static lra_status check_operand(const lra_operand *W) {
   if (!W) return fail(LRA_EINVAL, "null operand");
   if (W->m < 1 || W->n < 1) return fail(LRA_EINVAL, "empty operand (m=%lld, n=%lld)", (long long)W->m, (long long)W->n);
+  if (W->m_global < 0 || W->row0 < 0 || (W->m_global > 0 && W->row0 + W->m > W->m_global))
+    return fail(LRA_EINVAL, "bad row shard (row0 = %lld, m = %lld, m_global = %lld)", (long long)W->row0,
+                (long long)W->m, (long long)W->m_global);
+  if (W->m_global > 0 && W->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "only dense operands are row-sharded");
   if (W->kind == LRA_OP_DENSE) {
     if (!W->w) return fail(LRA_EINVAL, "dense operand with null w");
     if (W->ldw < W->m) return fail(LRA_EINVAL, "ldw < m");
@@ -203,8 +245,8 @@ const char *lra_last_error(void) { return g_err.c_str(); }
 lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_id, int nranks, int rank) {
   if (!h) return fail(LRA_EINVAL, "null handle pointer");
   *h = nullptr;
-  if (nccl_unique_id != nullptr || nranks != 1 || rank != 0)
-    return fail(LRA_EUNSUPPORTED, "in-library NCCL exchange is not in this build (nranks must be 1)");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LRA_EINVAL, "bad nranks / rank");
+  if (nranks > 1 && !nccl_unique_id) return fail(LRA_EINVAL, "nranks > 1 needs an NCCL unique id");
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
     cudaGetLastError();
@@ -219,7 +261,30 @@ lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_
   if (p->groups < 1) p->groups = 1;
   p->nranks = nranks;
   p->rank = rank;
+  p->comm = nullptr;
+  if (nccl_unique_id) {
+    if (!nccl().ok) {
+      delete p;
+      return fail(LRA_ENCCL, "libnccl.so.2 could not be loaded");
+    }
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclResult_t r = nccl().CommInitRank(&p->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete p;
+      return fail(LRA_ENCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+    }
+  }
   *h = p;
+  return LRA_OK;
+}
+
+lra_status lra_nccl_unique_id(void *out) {
+  if (!out) return fail(LRA_EINVAL, "null output");
+  if (!nccl().ok) return fail(LRA_ENCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NK(nccl().GetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
   return LRA_OK;
 }
 
@@ -228,6 +293,8 @@ void lra_handle_destroy(lra_handle h) {
   if (h->ws) cudaFree(h->ws);
   if (h->gs) cudaFree(h->gs);
   if (h->gm) cudaFree(h->gm);
+  if (h->sh) cudaFree(h->sh);
+  if (h->comm) nccl().CommDestroy(h->comm);
   for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
   if (h->streams_ready) {
     for (int i = 0; i < LRA_NSIDE; ++i) {
@@ -304,7 +371,8 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multipli
 static lra_status check_ca_shape(const lra_operand *W, int64_t r, int64_t k, int64_t l, int32_t sweeps) {
   if (k != l) return fail(LRA_EINVAL, "v1 requires k == l (reading C9)");
   if (r < 1 || r > k) return fail(LRA_EINVAL, "need 0 < r <= k");
-  if (k > W->m || l > W->n) return fail(LRA_EINVAL, "need k <= m and l <= n");
+  const int64_t mg = W->m_global > 0 ? W->m_global : W->m;
+  if (k > mg || l > W->n) return fail(LRA_EINVAL, "need k <= m and l <= n");
   if (k > LRA_QMAX_ALL) return fail(LRA_EUNSUPPORTED, "k > %d is outside this build's maxvol tiers", LRA_QMAX_ALL);
   if (sweeps < 1) return fail(LRA_EINVAL, "sweeps >= 1");
   return LRA_OK;
@@ -410,6 +478,202 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   return LRA_OK;
 }
 
+// ---------------------------------------------------------------- row-sharded C-A
+// One standalone maxvol (Alg D.2 stage 1 / D.1) on a dense fp64 block (N x q col-major):
+// cold (LUP) when start == nullptr, else warm from the slots `start`; slots -> out.
+static lra_status maxvol_block(lra_handle h, const double *blk, int64_t N, int q, const int64_t *start, int64_t *out,
+                               double tol, double tau, int32_t cap, lra_ca_stats *st_dev, int32_t *status,
+                               int64_t *dummyJ, cudaStream_t st) {
+  CAArgs ca{};
+  ca.op.kind = LRA_OP_DENSE;
+  ca.op.dtype = LRA_F64;
+  ca.op.m = N;
+  ca.op.n = N;
+  ca.op.w = blk;
+  ca.op.ldw = N;
+  ca.Y = blk;
+  ca.ldy = N;
+  ca.I0 = start;
+  ca.i0_stride = q;
+  ca.y_warm = start ? 1 : 0;
+  ca.q = q;
+  ca.qp = q | 1;
+  ca.sweeps = 0;
+  ca.cap = cap;
+  ca.tol = tol;
+  ca.tau = tau;
+  ca.I = out;
+  ca.J = dummyJ;
+  ca.stats = st_dev;
+  ca.status = status;
+  cudaError_t e;
+  const bool cluster = !ca_needs_global(N, q) && q <= 48 && N <= 16 * (q <= 24 ? 512 : 256);
+  if (cluster) {
+    int cs = 0;
+    e = launch_ca_cluster(ca, 1, N, st, &cs, &h->prof);
+  } else {
+    const size_t gb = ca_global_scratch_bytes(N, q);
+    if (h->gm_bytes < gb) {
+      if (h->gm) cudaFree(h->gm);
+      h->gm = nullptr;
+      h->gm_bytes = 0;
+      if (cudaMalloc(&h->gm, gb) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the global-memory C-A tier", gb);
+      }
+      h->gm_bytes = gb;
+    }
+    e = launch_ca_global(ca, 1, N, h->gm, st, &h->prof);
+  }
+  if (e == cudaErrorInvalidConfiguration) return fail(LRA_EUNSUPPORTED, "block %lld x %d exceeds the C-A tiers", (long long)N, q);
+  CK(e);
+  h->launches += 1;
+  return LRA_OK;
+}
+
+static lra_status allreduce_sum(lra_handle h, double *buf, size_t count, cudaStream_t st) {
+  if (h->nranks == 1 && !h->comm) return LRA_OK;
+  NK(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, h->comm, st));
+  return LRA_OK;
+}
+
+static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy,
+                                       const int64_t *I0, int64_t r, int64_t k, int32_t sweeps, double tol,
+                                       double tau, int32_t cap, int64_t *I, int64_t *J, double *U, double *A,
+                                       double *B, lra_ca_stats *stats, cudaStream_t st) {
+  if (!h->comm && h->nranks > 1) return fail(LRA_ENCCL, "row-sharded operand needs an NCCL communicator");
+  const int64_t M = W->m_global, n = W->n, q = k;
+  const int64_t Nmax = M > n ? M : n;
+  Carve probe{nullptr, 0};
+  probe.take<double>((size_t)Nmax * q);         // assembled block
+  probe.take<double>((size_t)n * q);            // R^T for the final factor B
+  probe.take<double>((size_t)q * q);            // G
+  probe.take<double>((size_t)q * r);            // TS
+  probe.take<double>((size_t)q * r);            // Sr
+  probe.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
+  probe.take<int32_t>(4);
+  probe.take<int64_t>((size_t)q);               // dummy J output of standalone maxvol calls
+  const size_t need = probe.off + 256;
+  if (h->sh_bytes < need) {
+    if (h->sh) cudaFree(h->sh);
+    h->sh = nullptr;
+    h->sh_bytes = 0;
+    if (cudaMalloc(&h->sh, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the sharded blocks", need);
+    }
+    h->sh_bytes = need;
+  }
+  Carve cv{(char *)h->sh, 0};
+  double *blk = cv.take<double>((size_t)Nmax * q);
+  double *Rt = cv.take<double>((size_t)n * q);
+  double *G = cv.take<double>((size_t)q * q);
+  double *TS = cv.take<double>((size_t)q * r);
+  double *Sr = cv.take<double>((size_t)q * r);
+  lra_ca_stats *sts = cv.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
+  int32_t *status = cv.take<int32_t>(4);
+  int64_t *dJ = cv.take<int64_t>((size_t)q);
+  const OpView op = make_view(W);                 // local rows (op.m = m_local)
+  lra_status s;
+  std::vector<lra_ca_stats> hs;
+  auto fetch = [&](int idx) -> lra_ca_stats {
+    lra_ca_stats x;
+    cudaMemcpyAsync(&x, sts + idx, sizeof(x), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return x;
+  };
+  CK(cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st));
+  // stage 2: I <- maxvol(Y) on the assembled m_global x lbar sketch, or the given I0
+  int nst = 0;
+  if (Y) {
+    CK(cudaMemsetAsync(blk, 0, (size_t)M * q * sizeof(double), st));
+    CK(launch_scatter_rows((const double *)Y, ldy, W->m, (int)q, W->row0, M, blk, st));
+    if ((s = allreduce_sum(h, blk, (size_t)M * q, st)) != LRA_OK) return s;
+    if ((s = maxvol_block(h, blk, M, (int)q, nullptr, I, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK) return s;
+    hs.push_back(fetch(nst++));
+    if (hs.back().status != LRA_OK) goto done;
+  } else {
+    CK(cudaMemcpyAsync(I, I0, q * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  }
+  for (int loop = 0; loop < sweeps; ++loop) {
+    // horizontal: J <- maxvol(W[I,:]^T) (cold in loop 0, else warm from J)
+    CK(cudaMemsetAsync(blk, 0, (size_t)n * q * sizeof(double), st));
+    CK(launch_scatter_wrows(op, I, (int)q, W->row0, blk, st));
+    if ((s = allreduce_sum(h, blk, (size_t)n * q, st)) != LRA_OK) return s;
+    if ((s = maxvol_block(h, blk, n, (int)q, loop ? J : nullptr, J, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK)
+      return s;
+    hs.push_back(fetch(nst++));
+    if (hs.back().status != LRA_OK) goto done;
+    // vertical: I <- maxvol(W[:,J]) warm from I
+    CK(cudaMemsetAsync(blk, 0, (size_t)M * q * sizeof(double), st));
+    CK(launch_scatter_wcols(op, J, (int)q, W->row0, M, blk, st));
+    if ((s = allreduce_sum(h, blk, (size_t)M * q, st)) != LRA_OK) return s;
+    if ((s = maxvol_block(h, blk, M, (int)q, I, I, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK) return s;
+    hs.push_back(fetch(nst++));
+    if (hs.back().status != LRA_OK) goto done;
+    if (loop > 0 && hs[hs.size() - 1].swaps == 0 && hs[hs.size() - 2].swaps == 0) break;   // reading C13
+  }
+  {
+    // nucleus and factors: G = W[I,J] and R = W[I,:] assembled, the replicated Jacobi SVD
+    CK(cudaMemsetAsync(Rt, 0, (size_t)n * q * sizeof(double), st));
+    CK(launch_scatter_wrows(op, I, (int)q, W->row0, Rt, st));
+    if ((s = allreduce_sum(h, Rt, (size_t)n * q, st)) != LRA_OK) return s;
+    CK(cudaMemsetAsync(G, 0, (size_t)q * q * sizeof(double), st));
+    CK(launch_scatter_g(op, I, J, (int)q, (int)q, W->row0, G, st));
+    if ((s = allreduce_sum(h, G, (size_t)q * q, st)) != LRA_OK) return s;
+    NucArgs na{};
+    na.op = op;
+    na.I = I;
+    na.J = J;
+    na.k = (int)q;
+    na.l = (int)q;
+    na.r = (int)r;
+    na.U = U;
+    na.TS = TS;
+    na.Sr = Sr;
+    na.status = status;
+    na.Gd = G;
+    FacArgs fa{};
+    fa.op = op;
+    fa.I = I;
+    fa.J = J;
+    fa.k = (int)q;
+    fa.l = (int)q;
+    fa.r = (int)r;
+    fa.TS = TS;
+    fa.Sr = Sr;
+    fa.A = A;
+    fa.B = B;
+    fa.status = status;
+    fa.Rt = Rt;
+    int nl = 0;
+    CK(launch_nucleus(na, fa, 1, st, &nl, &h->prof));
+    h->launches += nl;
+  }
+done:
+  if (stats) {   // combine the per-call statistics as the fused kernel reports them
+    lra_ca_stats out{};
+    out.status = LRA_OK;
+    int sw_last_h = 0;
+    for (size_t i = 0; i < hs.size(); ++i) {
+      const lra_ca_stats &x = hs[i];
+      if (x.status != LRA_OK) out.status = x.status;
+      out.lu_steps += x.lu_steps;
+      out.swaps += x.swaps;
+      out.cap_hits += x.cap_hits;
+      const bool is_y = Y && i == 0;
+      const size_t j = Y ? i - 1 : i;           // 0 = h, 1 = v, ...
+      if (is_y) out.sketch_swaps = x.swaps;
+      else if (j % 2 == 0) { out.cert_cols = x.cert_rows; sw_last_h = x.swaps; }
+      else { out.cert_rows = x.cert_rows; out.loops_done += 1; }
+    }
+    (void)sw_last_h;
+    CK(cudaMemcpyAsync(stats, &out, sizeof(out), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return LRA_OK;
+}
+
 lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy, int y_complex,
                             const int64_t *I0, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
                             double tie_slack, int32_t swap_cap, int64_t *I, int64_t *J, double *U, double *A,
@@ -423,6 +687,11 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
   if (!I || !J || !A || !B) return fail(LRA_EINVAL, "null output");
   if (!(swap_tol >= 0.0) || !(tie_slack >= 0.0) || tie_slack >= 1.0 || swap_cap < 0)
     return fail(LRA_EINVAL, "bad swap_tol / tie_slack / swap_cap");
+  if (W->m_global > 0) {
+    if (y_complex) return fail(LRA_EUNSUPPORTED, "ARFT sketches are not row-sharded in this build");
+    return sharded_cross_approx(h, W, Y, ldy, I0, r, k, sweeps, swap_tol, tie_slack, swap_cap, I, J, U, A, B,
+                                stats, (cudaStream_t)stream);
+  }
   Carve cv{nullptr, 0};
   size_t need = 0;
   {
@@ -456,6 +725,7 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   if (!A || !B || !num2 || !den2 || r < 1) return fail(LRA_EINVAL, "null A/B/num2/den2 or r < 1");
   cudaStream_t st = (cudaStream_t)stream;
   if (nsamples > 0) {
+    if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "the sampled estimate is not row-sharded");
     if (!si || !sj) return fail(LRA_EINVAL, "sampled residual needs si, sj");
     const int nblk = 296;
     if ((s = ws_reserve(h, (size_t)2 * nblk * sizeof(double2) + 256)) != LRA_OK) return s;
@@ -485,6 +755,10 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   } else {
     CK(launch_residual(a, 1, num2, den2, st, &nl, &h->prof));
   }
+  if (W->m_global > 0) {   // row-sharded: sum the partial norms over the ranks
+    if ((s = allreduce_sum(h, num2, 1, st)) != LRA_OK) return s;
+    if ((s = allreduce_sum(h, den2, 1, st)) != LRA_OK) return s;
+  }
   h->launches += nl;
   return LRA_OK;
 }
@@ -497,6 +771,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   if ((s = check_device(h)) != LRA_OK) return s;
   if ((s = check_operand(W0)) != LRA_OK) return s;
   if (W0->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "lra_batch needs dense blocks");
+  if (W0->m_global > 0) return fail(LRA_EINVAL, "lra_batch blocks are not row-sharded (deal blocks to ranks)");
   if (nb < 1) return fail(LRA_EINVAL, "nb >= 1");
   if (w_stride < W0->ldw * W0->n) return fail(LRA_EINVAL, "w_stride < ldw*n (blocks overlap)");
   if ((s = check_ca_shape(W0, r, k, l, sweeps)) != LRA_OK) return s;

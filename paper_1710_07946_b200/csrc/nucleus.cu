@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < L * k; e += NT) {
     int j = e / k, i = e % k;
-    G[e] = j < l ? op.at(I[i], J[j]) : 0.0;
+    G[e] = j < l ? (a.Gd ? a.Gd[(size_t)b * k * l + e] : op.at(I[i], J[j])) : 0.0;
   }
   for (int e = tid; e < L * L; e += NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
   __syncthreads();
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k_factor_B(FacArgs a) {
 #pragma unroll
   for (int u = 0; u < 16; ++u) acc[u] = 0.0;
   for (int s = 0; s < k; ++s) {
-    const double w = op.at(I[s], j);
+    const double w = a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j);
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       int t = chunk * 16 + u;

@@ -32,7 +32,8 @@ MUL_KIND = {"none": LRA_MUL_NONE, "gaussian": LRA_MUL_GAUSSIAN, "arht": LRA_MUL_
 class lra_operand(C.Structure):
     _fields_ = [("kind", C.c_int32), ("dtype", C.c_int32), ("m", C.c_int64), ("n", C.c_int64),
                 ("w", C.c_void_p), ("ldw", C.c_int64), ("fa", C.c_void_p), ("fb", C.c_void_p),
-                ("p", C.c_int64), ("e_rowptr", C.c_void_p), ("e_col", C.c_void_p), ("e_val", C.c_void_p)]
+                ("p", C.c_int64), ("e_rowptr", C.c_void_p), ("e_col", C.c_void_p), ("e_val", C.c_void_p),
+                ("row0", C.c_int64), ("m_global", C.c_int64)]
 
 
 class lra_multiplier(C.Structure):
@@ -73,6 +74,8 @@ def _load():
     lib.lra_batch.argtypes = [vp, i64, P(lra_operand), i64, P(lra_multiplier), i64, i64, i64, i64, i32, dbl, dbl,
                               i32, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.lra_last_error.restype = C.c_char_p
+    lib.lra_nccl_unique_id.argtypes = [vp]
+    lib.lra_nccl_unique_id.restype = C.c_int
     lib.lra_launch_count.argtypes = [vp]
     lib.lra_launch_count.restype = i64
     lib.lra_profile_enable.argtypes = [vp, C.c_int]
@@ -100,7 +103,7 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual"]
+            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id"]
 
 
 def debug_counters(reset=True):
@@ -142,18 +145,21 @@ def to_colmajor(W_np, device="cuda"):
 
 
 class Dense:
-    """A dense operand: Wt is (n, m) [or (nb, n, m) for batches], fp32 or fp64."""
+    """A dense operand: Wt is (n, m) [or (nb, n, m) for batches], fp32 or fp64.  A row shard
+    of an m_global x n matrix: rows [row0, row0 + m) with m_global > 0 (multi-GPU)."""
 
-    def __init__(self, Wt):
+    def __init__(self, Wt, row0=0, m_global=0):
         import torch
         assert Wt.is_cuda and Wt.is_contiguous() and Wt.dtype in (torch.float32, torch.float64)
         self.Wt = Wt
         self.n, self.m = Wt.shape[-2], Wt.shape[-1]
+        self.row0, self.m_global = int(row0), int(m_global)
 
     def struct(self):
         import torch
         return lra_operand(LRA_OP_DENSE, LRA_F32 if self.Wt.dtype == torch.float32 else LRA_F64,
-                           self.m, self.n, self.Wt.data_ptr(), self.m, None, None, 0, None, None, None)
+                           self.m, self.n, self.Wt.data_ptr(), self.m, None, None, 0, None, None, None,
+                           self.row0, self.m_global)
 
     def block_stride(self):
         return self.m * self.n
@@ -170,7 +176,7 @@ class Factored:
     def struct(self):
         return lra_operand(LRA_OP_FACTORED_CSR, LRA_F64, self.m, self.n, None, self.m, self.A_t.data_ptr(),
                            self.B_t.data_ptr(), self.p, self.row_ptr.data_ptr(), self.col.data_ptr(),
-                           self.val.data_ptr())
+                           self.val.data_ptr(), 0, 0)
 
 
 class Multiplier:
@@ -205,10 +211,21 @@ class Multiplier:
 
 
 # ------------------------------------------------------------------ the C-ABI, same names
+def nccl_unique_id():
+    """128-byte NCCL unique id (create on one rank, distribute with torch.distributed)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().lra_nccl_unique_id(buf))
+    return buf.raw
+
+
 class Handle:
-    def __init__(self, device=0):
+    """lra_handle_create: nccl_id (bytes from nccl_unique_id) + nranks/rank give the handle an
+    NCCL communicator for row-sharded operands; None for single-GPU use."""
+
+    def __init__(self, device=0, nccl_id=None, nranks=1, rank=0):
         h = C.c_void_p()
-        _check(lib().lra_handle_create(C.byref(h), int(device), None, 1, 0))
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(lib().lra_handle_create(C.byref(h), int(device), idbuf, int(nranks), int(rank)))
         self.h = h
 
     def close(self):

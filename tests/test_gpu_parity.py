@@ -372,3 +372,36 @@ def test_config5_recipe_downsized(P, h):
     M = synth.multiplier_abridged(0, n, 5, 96, "arht")
     rho, ora = _check_pipeline(P, h, np.asfortranarray(W), M, 64, 96, 3, rho_tol_rel=1e-4)
     assert 0.5 < rho < 1.0
+
+
+# ------------------------------------------------------------ row-sharded path (§8(e))
+def _sharded_run(P, W, mult, r, k, sweeps):
+    """The row-sharded entry points at one rank (a real NCCL communicator of size 1): every
+    block goes through the scatter + NCCL-sum assembly and the replicated standalone maxvol."""
+    from paper_1710_07946_b200 import pipeline
+    h1 = P.Handle(0, nccl_id=P.nccl_unique_id(), nranks=1, rank=0)
+    m, n = W.shape
+    Wd = P.lra.Dense(P.lra.to_colmajor(W), row0=0, m_global=m)
+    bufs = pipeline.cur(h1, Wd, P.lra.Multiplier(mult), r, k, sweeps)
+    torch.cuda.synchronize()
+    return bufs, P.lra.stats_to_numpy(bufs.stats)[0]
+
+
+@pytest.mark.parametrize("case", ["config2", "config5_small"])
+def test_sharded_path_one_rank_matches_oracle(P, case):
+    if case == "config2":      # cluster tier blocks
+        W = synth.config2(0)
+        mult, r, k = synth.multiplier_abridged(0, 4096, 4, 48, "arht"), 32, 48
+    else:                      # global tier blocks (q = 96)
+        W = synth.config5_torch(0, 8192, 8192).cpu().numpy().T
+        mult, r, k = synth.multiplier_abridged(0, 8192, 5, 96, "arht"), 64, 96
+    ora = O.cur_pipeline(W, mult, r, k, k, 3)
+    bufs, st = _sharded_run(P, np.asfortranarray(W), mult, r, k, 3)
+    assert st["status"] == 0
+    assert list(bufs.I.cpu().numpy()) == list(ora.I)
+    assert list(bufs.J.cpu().numpy()) == list(ora.J)
+    assert st["swaps"] == ora.ca.swaps and st["loops_done"] == ora.ca.loops_done
+    rho = float(np.sqrt(bufs.num2.item() / bufs.den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
+    U = bufs.U.cpu().numpy().T
+    assert np.allclose(U, ora.U, rtol=1e-9, atol=1e-9 * np.abs(ora.U).max())
