@@ -37,10 +37,32 @@ def test_library_exports_every_declared_symbol(L):
     assert set(L.EXPORTED) == set(_header_functions())
 
 
-def test_struct_layouts(L):
-    assert ctypes.sizeof(L.lra_operand) == 4 + 4 + 8 * 10
-    assert ctypes.sizeof(L.lra_multiplier) == 4 + 4 + 8 * 5 + 4 + 4 + 8 + 8
-    assert L.STATS_DTYPE.itemsize == 40
+def test_struct_layouts(L, tmp_path):
+    """The ctypes mirrors of the C structs match include/lra.h field by field: a C program
+    compiled against the header prints every size and offset (gcc, no CUDA needed)."""
+    import subprocess
+    fields = {"lra_operand": [f for f, _ in L.lra_operand._fields_],
+              "lra_multiplier": [f for f, _ in L.lra_multiplier._fields_],
+              "lra_ca_stats": list(L.STATS_DTYPE.names)}
+    src = ["#include <stdio.h>", "#include <stddef.h>", '#include "lra.h"', "int main(void) {"]
+    for st, fs in fields.items():
+        src.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            src.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    src.append("return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for st, cls in (("lra_operand", L.lra_operand), ("lra_multiplier", L.lra_multiplier)):
+        assert int(got[st]) == ctypes.sizeof(cls), st
+        for f, _ in cls._fields_:
+            assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
+    assert int(got["lra_ca_stats"]) == L.STATS_DTYPE.itemsize
+    for f in L.STATS_DTYPE.names:
+        assert int(got[f"lra_ca_stats.{f}"]) == L.STATS_DTYPE.fields[f][1], f"lra_ca_stats.{f}"
 
 
 def test_no_cpu_fallback(L):
