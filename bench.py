@@ -167,6 +167,8 @@ def algorithmic(name, mult, B):
         return B * (m * (1 << DEPTH) * fibers * 4 + m * K * 8), 0.0
     if name == "k_residual":
         return B * (m * n * 4 + (m * R + R * n) * 8), B * 2.0 * m * n * R
+    if name == "k_residual_tc":   # W once + the int8 digit slices of A and B (6 each)
+        return B * (m * n * 4 + (m + n) * R * 6), B * 2.0 * m * n * R * 21
     if name == "k_ca":
         return B * SWEEPS * (m * K + K * n) * 4, 0.0
     return 0, 0.0
@@ -177,7 +179,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=28)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -251,7 +253,16 @@ def main():
     name, (kms, cnt) = dom
     per_launch_s = kms / cnt / 1e3
     byts, flops = algorithmic(name, mult, B)
-    if name == "k_residual":
+    if name == "k_ca":
+        ach = byts / per_launch_s / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src, "traffic": None,
+                "note": "latency-bound pivot chain (DESIGN.md §6.1): the algorithmic gather bytes over the launch "
+                        "time; see 'latency' for the per-step cost",
+                "latency": {"launch_ms": kms / cnt, "matrices_per_launch": B / max(1, cnt // max(1, args.steps)),
+                            "pivot_steps_per_matrix": float(np.mean(stats["lu_steps"] + stats["swaps"])),
+                            "us_per_pivot_step": kms / cnt * 1e3 / max(1.0, float(np.mean(stats["lu_steps"] + stats["swaps"])))}}
+    elif name == "k_residual":
         fp64_peak = float(os.environ.get("LRA_FP64_TFLOPS", "37.2"))
         roof = {"kernel": name, "bound": "alu", "achieved": flops / per_launch_s / 1e12, "peak": fp64_peak,
                 "unit": "TFLOP/s", "frac": flops / per_launch_s / 1e12 / fp64_peak,
@@ -265,7 +276,7 @@ def main():
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1],
                    "share": v[0] / sum(x[0] for x in prof.values())} for k, v in prof.items()}
     stage_gbs = {}
-    for k in ("k_sketch_arht", "k_residual"):
+    for k in ("k_sketch_arht", "k_residual", "k_residual_tc"):
         if k in prof:
             b, _ = algorithmic(k, mult, B)
             stage_gbs[k] = b / (prof[k][0] / prof[k][1] / 1e3) / 1e9

@@ -732,6 +732,47 @@ static cudaError_t launch_cc_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   return e;
 }
 
+template <int Q, int TPR>
+static int cc_active_t(int64_t maxN) {
+  constexpr int RPC = ccl::NT / TPR;
+  int cs = 1;
+  while ((int64_t)cs * RPC < maxN) cs *= 2;
+  if (cs > 16) return 0;
+  const int rpc = (int)((maxN + cs - 1) / cs);
+  const size_t smem = cc_smem(rpc, Q);
+  void (*kern)(CAArgs) = ccl::k_cacl<Q, TPR, 0>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(cs * 64));
+  cfg.blockDim = dim3(ccl::NT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// Problems of this shape the cluster tier runs concurrently (co-resident clusters; 0 if the
+// tier does not apply).  B200, config 2 (16-CTA clusters): 7.
+int ca_cluster_max_active(int64_t maxN, int q) {
+  if (q <= 8) return cc_active_t<8, 1>(maxN);
+  if (q <= 16) return cc_active_t<16, 1>(maxN);
+  if (q <= 24) return cc_active_t<24, 1>(maxN);
+  if (q <= 32) return cc_active_t<32, 2>(maxN);
+  if (q <= 48) return cc_active_t<48, 2>(maxN);
+  return 0;
+}
+
 // Cluster tier of the real C-A (q <= 48, at most 16 CTAs of NT / TPR rows): returns
 // cudaErrorInvalidConfiguration when the problem does not fit (caller falls back).
 cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {

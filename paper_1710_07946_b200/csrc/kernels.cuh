@@ -74,6 +74,7 @@ cudaError_t read_ca_counters(unsigned long long *out, bool reset);
 // cluster tier of the real C-A (ca_cluster.cu); cudaErrorInvalidConfiguration if it does not fit
 cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
 cudaError_t read_cc_counters(unsigned long long *out, bool reset);
+int ca_cluster_max_active(int64_t maxN, int q);
 // global-memory tier (ca_global.cu): any N, q <= 128; scratch ca_global_scratch_bytes
 size_t ca_global_scratch_bytes(int64_t maxN, int q);
 cudaError_t launch_ca_global(CAArgs a, int64_t nb, int64_t maxN, void *scratch, cudaStream_t st, Prof *pf);

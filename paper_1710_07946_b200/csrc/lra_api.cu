@@ -70,7 +70,7 @@ static lra_status fail(lra_status s, const char *fmt, ...) {
 #define LRA_NSIDE 8
 struct lra_handle_s {
   int device;
-  int groups;                     // lra_batch groups (env LRA_BATCH_GROUPS, default 2)
+  int groups_env;                 // lra_batch groups from env LRA_BATCH_GROUPS (0: automatic)
   cudaStream_t side[LRA_NSIDE];
   cudaEvent_t fork, join[LRA_NSIDE];
   bool streams_ready;
@@ -257,8 +257,8 @@ lra_status lra_handle_create(lra_handle *h, int device, const void *nccl_unique_
   lra_handle_s *p = new lra_handle_s();
   p->device = device;
   const char *g = getenv("LRA_BATCH_GROUPS");
-  p->groups = g ? atoi(g) : 2;
-  if (p->groups < 1) p->groups = 1;
+  p->groups_env = g ? atoi(g) : 0;
+  if (p->groups_env < 0) p->groups_env = 0;
   p->nranks = nranks;
   p->rank = rank;
   p->comm = nullptr;
@@ -813,7 +813,18 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   // events, so the call stays stream-ordered and graph-capturable): the latency-bound C-A
   // and nucleus of one group overlap the bandwidth-bound sketch/residual of another.
   if ((s = ensure_streams(h)) != LRA_OK) return s;
-  int64_t ngroups = nb < h->groups ? nb : h->groups;
+  // Group size: as many problems as the cluster tier runs concurrently (one wave of co-resident
+  // clusters; 7 for config 2 on a B200), so that one group's C-A fills the GPCs while the
+  // previous group's nucleus / residual use the remaining SMs.  LRA_BATCH_GROUPS overrides.
+  int64_t ngroups;
+  if (h->groups_env > 0) {
+    ngroups = nb < h->groups_env ? nb : h->groups_env;
+  } else {
+    const int act = ca_cluster_max_active(m > n ? m : n, (int)k);
+    const int64_t per = act >= 2 ? act : 4;
+    ngroups = (nb + per - 1) / per;
+    if (ngroups < 1) ngroups = 1;
+  }
   const int64_t gsz = (nb + ngroups - 1) / ngroups;
   ngroups = (nb + gsz - 1) / gsz;
   CK(cudaEventRecord(h->fork, st));

@@ -9,8 +9,8 @@ tail -3 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py ${BENCH_EXTRA} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench=$?"
 cat gpurun_out/bench.json | head -c 3000
 if [ -z "$NO_NCU" ]; then
-P="python bench.py --profile-only --steps 1 --warmup 1 --batch 16"
+P="python bench.py --profile-only --steps 1 --warmup 1 --batch 14"
 timeout 300 $P > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1; echo "ncu_launch=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${NCU_K:-k_ca|k_residual|k_sketch|k_nucleus|k_factors}" -s ${NCU_S:-0} -c ${NCU_C:-5} -f -o gpurun_out/prof $P > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${NCU_K:-k_cacl|k_residual_tc|k_sketch|k_nucleus|k_split}" -s ${NCU_S:-0} -c ${NCU_C:-5} -f -o gpurun_out/prof $P > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
 fi
