@@ -252,14 +252,16 @@ def main():
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     name, (kms, cnt) = dom
     per_launch_s = kms / cnt / 1e3
-    byts, flops = algorithmic(name, mult, B)
+    # one launch processes one batch group: B * steps / (launches of this kernel in the region)
+    per_launch_mats = B * args.steps / cnt
+    byts, flops = algorithmic(name, mult, per_launch_mats)
     if name == "k_ca":
         ach = byts / per_launch_s / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src, "traffic": None,
                 "note": "latency-bound pivot chain (DESIGN.md §6.1): the algorithmic gather bytes over the launch "
                         "time; see 'latency' for the per-step cost",
-                "latency": {"launch_ms": kms / cnt, "matrices_per_launch": B / max(1, cnt // max(1, args.steps)),
+                "latency": {"launch_ms": kms / cnt, "matrices_per_launch": per_launch_mats,
                             "pivot_steps_per_matrix": float(np.mean(stats["lu_steps"] + stats["swaps"])),
                             "us_per_pivot_step": kms / cnt * 1e3 / max(1.0, float(np.mean(stats["lu_steps"] + stats["swaps"])))}}
     elif name == "k_residual":
@@ -278,7 +280,7 @@ def main():
     stage_gbs = {}
     for k in ("k_sketch_arht", "k_residual", "k_residual_tc"):
         if k in prof:
-            b, _ = algorithmic(k, mult, B)
+            b, _ = algorithmic(k, mult, B * args.steps / prof[k][1])
             stage_gbs[k] = b / (prof[k][0] / prof[k][1] / 1e3) / 1e9
 
     # ---- e2e through the public API with host buffers (H2D of W, D2H of results, timed)

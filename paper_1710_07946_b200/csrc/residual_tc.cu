@@ -31,6 +31,9 @@ __device__ unsigned long long g_rtc_cyc[16];
 #define RTC_PROF 0      // 1: per-role clock64 counters (lra_debug_counters_residual)
 #endif
 #define RTC_CLK() (RTC_PROF ? clock64() : 0ll)
+#ifndef RTC_EPI_LDONLY
+#define RTC_EPI_LDONLY 0   // 1: epilogue reads TMEM but skips the arithmetic (diagnostics)
+#endif
 namespace rtc {
 
 constexpr int BM = 128;        // rows per CTA (MMA M)
@@ -56,6 +59,13 @@ __device__ __forceinline__ void digits(double x, int e, int S, signed char *d) {
     d[s] = (signed char)(int)q;
     y -= q;
   }
+}
+
+__device__ __forceinline__ unsigned long long wmax_bits(unsigned long long k) {   // max over the warp
+  const unsigned hi = (unsigned)(k >> 32);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned)k : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
 }
 
 __device__ __forceinline__ int scale_exp(double mx) {
@@ -117,7 +127,7 @@ __global__ void __launch_bounds__(64) k_split_a(const double *A, int64_t m, int 
 }
 
 // B: r x n (ld r), per problem stride b_stride.  Output Bq[((b * CB + cb) * KB + kb) * S + s][B_TILE]
-// and sbq[(b * CB + cb) * BN + jj] = fb_j (int32; -4000 beyond n).  grid (CB, nb), 64 threads.
+// and sbq[(b * CB + cb) * BN + jj] = fb of the tile (int32; -4000 beyond n).  grid (CB, nb), 64 threads.
 __global__ void __launch_bounds__(2 * BN) k_split_b(const double *B, int64_t n, int r, int64_t b_stride, int S, int KB,
                                                     signed char *Bq, int *sbq, const int32_t *status) {
   const int64_t b = blockIdx.y, cb = blockIdx.x;
@@ -127,10 +137,13 @@ __global__ void __launch_bounds__(2 * BN) k_split_b(const double *B, int64_t n, 
   const int64_t gj = cb * BN + jj;
   const bool ok = gj < n && !(status && status[b] != LRA_OK);
   const double *Bb = B + b * b_stride;
-  const double mx = ok ? strided_absmax(Bb + gj * r, 1, r) : 0.0;
+  // one exponent per 32-column tile (the tile's max |B|): the epilogue then builds one scale
+  // per row and tile instead of one per output
+  const double mxc = ok ? strided_absmax(Bb + gj * r, 1, r) : 0.0;
+  const double mx = __longlong_as_double((long long)wmax_bits((unsigned long long)__double_as_longlong(mxc)));
   const int e = scale_exp(mx);
   const double p2 = ldexp(1.0, -e);
-  if (h == 0) sbq[(b * CB + cb) * BN + jj] = ok ? e : -4000;
+  if (h == 0) sbq[(b * CB + cb) * BN + jj] = ok ? e : -4000;   // (same e for the tile's columns)
   for (int kb = 0; kb < KB; ++kb) {
     uint32_t w[SMAX][4];
 #pragma unroll
@@ -189,6 +202,7 @@ __device__ __forceinline__ void cp16(void *s, const void *g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait2() { asm volatile("cp.async.wait_group 2;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
@@ -239,12 +253,14 @@ struct TcArgs {
   int tpi;                        // 32-column tiles per work item
   int64_t nchunk;                 // column chunks (items) per row block
   int64_t items;                  // nb * RB * nchunk
+  int nst, wring;                 // B-slice stages (<= NST) and W ring depth (2 or 3) fitting smem
   double2 *partial;               // per problem: RB * nchunk partials (one per item)
   const int32_t *status;
 };
 
-constexpr int NST = 6;            // B-slice stages
-constexpr int NEPI = 16;          // epilogue warps (warp w: TMEM lanes 32 (w % 4), columns 8 (w / 4) ..)
+constexpr int NST = 6;            // max B-slice stages
+constexpr int NEPI = 16;          // epilogue warps: two groups of 8 own alternate tiles (= TMEM buffers);
+                                  // warp w: TMEM lanes 32 (w % 4), columns 16 ((w / 4) % 2) ..
 constexpr int NTC = 32 * (NEPI + 2);   // + producer warp + MMA warp
 constexpr int WRING = 3;          // per-warp W ring depth (tiles)
 
@@ -264,7 +280,7 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
   const int stBytes = bBytes;
   unsigned char *As = smem;                            // 2 item buffers
   unsigned char *Bst = smem + 2 * aBytes;              // NST stages
-  TW *Wr = reinterpret_cast<TW *>(Bst + NST * stBytes);   // NEPI x WRING x 8 cols x 32 rows
+  TW *Wr = reinterpret_cast<TW *>(Bst + a.nst * stBytes);   // NEPI x WRING x 16 cols x 32 rows
   const uint32_t bb = smem_u32(&bar);
   const uint32_t B_BFULL = bb + offsetof(Bars, bfull), B_BEMPTY = bb + offsetof(Bars, bempty);
   const uint32_t B_TFULL = bb + offsetof(Bars, tfull), B_TEMPTY = bb + offsetof(Bars, tempty);
@@ -274,13 +290,13 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < a.nst; ++i) {
       mbar_init(B_BFULL + 8 * i, 1);
       mbar_init(B_BEMPTY + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(B_TFULL + 8 * i, 1);
-      mbar_init(B_TEMPTY + 8 * i, NEPI);
+      mbar_init(B_TEMPTY + 8 * i, NEPI / 2);   // released by the 8 warps of its group
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(B_AFULL + 8 * i, 1);
@@ -323,9 +339,9 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
         }
         __syncwarp();
         for (int64_t ct = c0; ct < c1; ++ct, ++k) {
-          const int st = (int)(k % NST);
+          const int st = (int)(k % a.nst);
           long long t0 = RTC_CLK();
-          if (k >= NST) mbar_wait(B_BEMPTY + 8 * st, (uint32_t)(((k / NST) - 1) & 1));
+          if (k >= a.nst) mbar_wait(B_BEMPTY + 8 * st, (uint32_t)(((k / a.nst) - 1) & 1));
           pw_b += RTC_CLK() - t0;
           if (elect_one()) {
             mbar_expect(B_BFULL + 8 * st, (uint32_t)stBytes);
@@ -355,9 +371,9 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
         mw_a += RTC_CLK() - t0;
         ++ni;
         for (int64_t ct = c0; ct < c1; ++ct, ++k) {
-          const int st = (int)(k % NST), tb = (int)(k & 1);
+          const int st = (int)(k % a.nst), tb = (int)(k & 1);
           long long t1 = RTC_CLK();
-          mbar_wait(B_BFULL + 8 * st, (uint32_t)((k / NST) & 1));
+          mbar_wait(B_BFULL + 8 * st, (uint32_t)((k / a.nst) & 1));
           long long t2 = RTC_CLK();
           if (k >= 2) mbar_wait(B_TEMPTY + 8 * tb, (uint32_t)(((k >> 1) - 1) & 1));
           long long t3 = RTC_CLK();
@@ -404,12 +420,15 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
       }
     }
   } else {
-    // ===== epilogue warps: warp w drains TMEM lanes 32 (w % 4).. (its 32 rows) x the 8
-    // columns 8 (w / 4).. of every tile; its W values come through a private cp.async ring.
-    const int q4 = warp & 3, cg8 = warp >> 2;
+    // ===== epilogue warps.  Group g = warp / 8 handles the tiles k with k % 2 == g (TMEM buffer
+    // g): while one group reads its accumulators (TMEM-read bound) the other one computes, so
+    // the two phases overlap.  Warp w drains TMEM lanes 32 (w % 4).. (its 32 rows) x the 16
+    // columns 16 ((w / 4) % 2).. of its tiles; W comes through a private cp.async ring.
+    const int q4 = warp & 3, half = (warp >> 2) & 1, grp = warp >> 3;
     const int rl = 32 * q4 + lane;                     // row within the block (TMEM lane)
-    TW *ring = Wr + (size_t)warp * WRING * 8 * 32;
-    const uint32_t lane_addr = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(8 * cg8);
+    const int WR = a.wring;
+    TW *ring = Wr + (size_t)warp * WR * 16 * 32;
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(16 * half);
     const TW *Wg = reinterpret_cast<const TW *>(a.w);
     constexpr int PER = 16 / (int)sizeof(TW);          // elements per 16-byte chunk
     int64_t k = 0;
@@ -421,97 +440,110 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
       const TW *W = Wg + b * a.w_stride;
       const int64_t row0 = rb * BM;
       const int64_t gi = row0 + rl;
-      // scale of R in 2^(ea_i + fb_j + es): es = -35 - 7 (S = 6) / -35 + 7 (S = 3); exponent
-      // field of the double 2^(ea_i + fb_j + es) built directly (rows / columns outside the
-      // problem carry -4000 and give a zero scale)
+      // scale of R in 2^(ea_i + fb_tile + es): es = -35 - 7 (S = 6) / -35 + 7 (S = 3); exponent
+      // field of the double built directly (rows / columns outside the problem carry -4000)
       const int eai = (gi < a.m ? a.sa[b * a.m + gi] : -4000) + (S == 6 ? -42 : -28) + 1023;
-      const int *sbcol = a.sbq + b * a.CB * BN + 8 * cg8;
-      int fbn[8];
-#pragma unroll
-      for (int x = 0; x < 8; ++x) fbn[x] = __ldg(sbcol + c0 * BN + x);
+      const int *sbcol = a.sbq + b * a.CB * BN;
       const bool vec_ok = ((a.ldw * (int64_t)sizeof(TW)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0) &&
                           row0 + BM <= a.m;
-      auto load_w = [&](int64_t ct) {
-        TW *dst = ring + (int)((ct - c0) % WRING) * 8 * 32;
-        const int64_t cb0 = ct * BN + 8 * cg8;
-        if (vec_ok && cb0 + 8 <= a.n) {
-          for (int e = lane; e < 8 * 32 / PER; e += 32) {
+      // the tiles of this group inside the item: global tile counter k + (ct - c0) must match grp
+      const int64_t first = c0 + (int64_t)(((k & 1) != grp) ? 1 : 0);
+      auto load_w = [&](int64_t ct, int slot) {
+        TW *dst = ring + slot * 16 * 32;
+        const int64_t cb0 = ct * BN + 16 * half;
+        if (vec_ok && cb0 + 16 <= a.n) {
+          for (int e = lane; e < 16 * 32 / PER; e += 32) {
             const int c = e / (32 / PER), r4 = (e % (32 / PER)) * PER;
             cp16(dst + c * 32 + r4, W + (cb0 + c) * a.ldw + row0 + 32 * q4 + r4);
           }
         } else {
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 16; ++c) {
             const int64_t gj = cb0 + c;
             dst[c * 32 + lane] = (gi < a.m && gj < a.n) ? W[gj * a.ldw + gi] : (TW)0;
           }
         }
       };
-      for (int64_t j = 0; j < WRING - 1; ++j) {
-        if (c0 + j < c1) load_w(c0 + j);
+      int slot_ld = 0, slot_use = 0;
+      for (int j = 0; j < WR - 1; ++j) {
+        const int64_t ct = first + 2 * j;
+        if (ct < c1) load_w(ct, slot_ld);
         cp_commit();
+        slot_ld = (slot_ld + 1) % WR;
       }
       double num = 0.0, den = 0.0;
-      for (int64_t ct = c0; ct < c1; ++ct, ++k) {
-        if (ct + WRING - 1 < c1) load_w(ct + WRING - 1);
-        cp_commit();
-        const int tb = (int)(k & 1);
-        int fbc[8];
-#pragma unroll
-        for (int x = 0; x < 8; ++x) fbc[x] = fbn[x];
-        if (ct + 1 < c1) {                               // prefetch the next tile's column exponents
-#pragma unroll
-          for (int x = 0; x < 8; ++x) fbn[x] = __ldg(sbcol + (ct + 1) * BN + x);
+      for (int64_t ct = first; ct < c1; ct += 2) {
+        const int64_t kk = k + (ct - c0);               // global tile counter (parity == grp)
+        {
+          const int64_t cn = ct + 2 * (WR - 1);
+          if (cn < c1) load_w(cn, slot_ld);
+          cp_commit();
+          slot_ld = (slot_ld + 1) % WR;
         }
+        const int tb = (int)(kk & 1);
+        const int ex = eai + __ldg(sbcol + ct * BN);    // scale of this tile
+        const double sc = ex > 0 ? __hiloint2double(ex << 20, 0) : 0.0;
         long long te0 = RTC_CLK();
-        mbar_wait(B_TFULL + 8 * tb, (uint32_t)((k >> 1) & 1));
+        mbar_wait(B_TFULL + 8 * tb, (uint32_t)((kk >> 1) & 1));
         long long te1 = RTC_CLK();
         ew_t += te1 - te0;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint32_t P[S][8];
-#pragma unroll
-        for (int l = 0; l < S; ++l)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(P[l][0]), "=r"(P[l][1]), "=r"(P[l][2]), "=r"(P[l][3]), "=r"(P[l][4]), "=r"(P[l][5]),
-                         "=r"(P[l][6]), "=r"(P[l][7])
-                       : "r"(lane_addr + (uint32_t)(tb * 192 + l * BN)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        long long te2 = RTC_CLK();
-        ew_ld += te2 - te1;
-#pragma unroll
-        for (int l = 0; l < S; ++l)   // register dependence on the wait: no use before it
-          asm volatile("" : "+r"(P[l][0]), "+r"(P[l][1]), "+r"(P[l][2]), "+r"(P[l][3]), "+r"(P[l][4]),
-                       "+r"(P[l][5]), "+r"(P[l][6]), "+r"(P[l][7]));
-        // TMEM buffer consumed: release it to the MMA warp before the arithmetic
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        if (WR == 3) cp_wait2(); else cp_wait1();
         __syncwarp();
-        if (lane == 0) mbar_arrive(B_TEMPTY + 8 * tb);
-        long long te3 = RTC_CLK();
-        cp_wait2();
-        __syncwarp();
-        ew_w += RTC_CLK() - te3;
-        const TW *wt = ring + (int)((ct - c0) % WRING) * 8 * 32;
+        const TW *wt = ring + slot_use * 16 * 32;
+        slot_use = (slot_use + 1) % WR;
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const double w = (double)wt[x * 32 + lane];
-          // R = sum_l P_l 2^(7 (S-1-l)) exactly in int64 (the last level's low 7 bits dropped for
-          // S = 6: < 2^-47 of the scale, below the 2^-42 truncation); units of 2^7 (S=6) / 1 (S=3)
-          long long R;
-          if (S == 6) {
-            const int lo = (int)P[3][x] * 128 + (int)P[4][x] + ((int)P[5][x] >> 7);
-            R = (long long)(int)P[2][x] * 16384 + lo;
-            R += (long long)(int)P[1][x] * 2097152;
-            R += (long long)(int)P[0][x] * 268435456;
-          } else {
-            R = (long long)((int)P[0][x] * 128 + (int)P[1][x]) * 128 + (int)P[2][x];
+        for (int cc = 0; cc < 16; cc += 8) {
+          uint32_t P[S][8];
+#pragma unroll
+          for (int l = 0; l < S; ++l)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(P[l][0]), "=r"(P[l][1]), "=r"(P[l][2]), "=r"(P[l][3]), "=r"(P[l][4]), "=r"(P[l][5]),
+                           "=r"(P[l][6]), "=r"(P[l][7])
+                         : "r"(lane_addr + (uint32_t)(tb * 192 + l * BN + cc)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int l = 0; l < S; ++l)   // register dependence on the wait: no use before it
+            asm volatile("" : "+r"(P[l][0]), "+r"(P[l][1]), "+r"(P[l][2]), "+r"(P[l][3]), "+r"(P[l][4]),
+                         "+r"(P[l][5]), "+r"(P[l][6]), "+r"(P[l][7]));
+          if (cc == 8) {   // both chunks read: release the TMEM buffer to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(B_TEMPTY + 8 * tb);
           }
-          const double ab = i64_to_f64(R);
-          const int ex = eai + fbc[x];
-          const double sc = ex > 0 ? __hiloint2double(ex << 20, 0) : 0.0;
-          const double d = fma(-ab, sc, w);
-          num = fma(d, d, num);
-          den = fma(w, w, den);
+          ew_ld += RTC_CLK() - te1;
+#if RTC_EPI_LDONLY
+          {
+            unsigned acc = 0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+#pragma unroll
+              for (int l = 0; l < S; ++l) acc ^= P[l][x];
+            num += (double)acc;
+          }
+          if (false)
+#endif
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const double w = (double)wt[(cc + x) * 32 + lane];
+            // R = sum_l P_l 2^(7 (S-1-l)) exactly in int64 (the last level's low 7 bits dropped
+            // for S = 6: < 2^-47 of the scale, below the 2^-42 truncation)
+            long long R;
+            if (S == 6) {
+              const int lo = (int)P[3][x] * 128 + (int)P[4][x] + ((int)P[5][x] >> 7);
+              R = (long long)(int)P[2][x] * 16384 + lo;
+              R += (long long)(int)P[1][x] * 2097152;
+              R += (long long)(int)P[0][x] * 268435456;
+            } else {
+              R = (long long)((int)P[0][x] * 128 + (int)P[1][x]) * 128 + (int)P[2][x];
+            }
+            const double ab = i64_to_f64(R);
+            const double d = fma(-ab, sc, w);
+            num = fma(d, d, num);
+            den = fma(w, w, den);
+          }
         }
       }
+      k += c1 - c0;
       cp_wait0();
       // item partial: sum over the epilogue warps (fixed order) -> partial[item]
       num = warp_sum(num);
@@ -617,8 +649,20 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
   t.items = nb * RB * t.nchunk;
   t.partial = a.partial;
   t.status = a.status;
-  const size_t wbytes = (size_t)NEPI * WRING * 8 * 32 * (a.dtype == LRA_F32 ? 4 : 8);
-  const size_t smem = 2 * (size_t)S * KB * A_TILE + NST * ((size_t)S * KB * B_TILE) + wbytes;
+  // shared memory: 2 A buffers + nst B stages + the per-warp W rings; shrink the B stages and
+  // then the W ring until it fits (r > 32 needs two K blocks)
+  const size_t elt = a.dtype == LRA_F32 ? 4 : 8;
+  const size_t limit = 227 * 1024 - 2048;
+  t.nst = NST;
+  t.wring = WRING;
+  auto smem_of = [&](int nst, int wr) {
+    return 2 * (size_t)S * KB * A_TILE + (size_t)nst * S * KB * B_TILE + (size_t)NEPI * wr * 16 * 32 * elt;
+  };
+  while (smem_of(t.nst, t.wring) > limit && t.nst > 3) --t.nst;
+  if (smem_of(t.nst, t.wring) > limit) t.wring = 2;
+  while (smem_of(t.nst, t.wring) > limit && t.nst > 2) --t.nst;
+  if (smem_of(t.nst, t.wring) > limit) return cudaErrorInvalidConfiguration;
+  const size_t smem = smem_of(t.nst, t.wring);
   const int64_t grid = t.items < num_sms_rtc() ? t.items : num_sms_rtc();
   pf->begin("k_residual_tc", st);
   void (*kern)(TcArgs) = a.dtype == LRA_F32 ? (S == 6 ? k_residual_tc<float, 6> : k_residual_tc<float, 3>)
