@@ -71,6 +71,35 @@ def sketch(W: np.ndarray, mult: dict) -> np.ndarray:
     raise ValueError(kind)
 
 
+def preprocess_full(W: np.ndarray, mult: dict) -> np.ndarray:
+    """Alg 10.1 stage 1 with u = n and the abridged randomized Hadamard multiplier
+    (the Table tb_fh protocol P:4882-4914):
+    W' = W·D·H_{n,d}·P with ALL n columns, column c = (W D H_{n,d})[:, perm[c]] — the same
+    ascending-t signed sum as `sketch` with lbar = n — stored in W's precision (reading C25:
+    fp32 W -> fl32 of the fp64 sum, fp64 W -> the fp64 sum)."""
+    W = np.asarray(W)
+    if mult["kind"] != "arht" or mult["lbar"] != W.shape[1]:
+        raise ValueError("full pre-processing: ARHT multiplier with lbar = n")
+    Wp = sketch(W, mult)
+    return Wp.astype(np.float32) if W.dtype == np.float32 else Wp
+
+
+def cur_preprocessed(W, mult_full, r: int, k: int, sweeps: int, I0):
+    """Alg 10.1 with C-A as its CUR subalgorithm (the Table tb_fh protocol, P:4882-4914;
+    SURVEY NEXT-1): W' = W·D·H_{n,d}·P, C-A ("Tests 2": random I0) and the
+    canonical nucleus on W', so C = W'[:,J], U = W'_{k,l,r}^+ and R = R_H·H^+ = W[I,:]
+    (R = R_H H^+, H square and invertible).  The relative residual on W' equals the
+    one on W because M M^T = 2^d I (so ||X M||_F = 2^{d/2} ||X||_F).  Returns the CurResult
+    on W' and rho_W = ||W - C U W[I,:]||_F / ||W||_F computed directly."""
+    Wp = preprocess_full(W, mult_full)
+    res = cur_pipeline(Wp, None, r, k, k, sweeps, I0=I0)
+    Wd = np.asarray(W, dtype=np.float64)
+    C = np.asarray(Wp, dtype=np.float64)[:, res.J]
+    D = Wd - C @ res.U @ Wd[res.I, :]
+    rho_w = float(np.sqrt(np.sum(D * D) / np.sum(Wd * Wd)))
+    return res, rho_w
+
+
 # ====================================================== maxvol (Alg D.2 + Alg D.1)
 @dataclass
 class MaxvolResult:

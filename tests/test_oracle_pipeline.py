@@ -168,3 +168,44 @@ def test_factored_entries_vectorized():
         Wd[i, c4["col"][lo:hi]] += c4["val"][lo:hi]
     ii, jj = synth.sample_pairs(3, 300, 250, 5000)
     assert np.allclose(op.entries(ii, jj), Wd[ii, jj], atol=1e-14)
+
+
+# ------------------------------------------------------------ NEXT-1: Alg 10.1 full pre-processing
+def test_preprocess_full_equals_dense_hadamard_product():
+    """d = log2 n: W' = W·D·H_n·P with the Sylvester Hadamard matrix from scipy (a library
+    routine, not the oracle's recursion); integer-valued W so every sum is exact and the fp32
+    rounding is the identity."""
+    import scipy.linalg
+    g = np.random.default_rng(3)
+    n, d = 64, 6
+    W = g.integers(-50, 50, size=(37, n)).astype(np.float32)
+    mult = synth.multiplier_abridged(2, n, d, n, "arht")
+    H = scipy.linalg.hadamard(n).astype(np.float64)
+    M = (mult["dsign"].astype(np.float64)[:, None] * H)[:, mult["col"]]
+    ref = (W.astype(np.float64) @ M).astype(np.float32)
+    assert np.array_equal(lra.preprocess_full(W, mult), ref)
+
+
+def test_preprocess_full_norm_and_abridged_blocks():
+    """d < log2 n (n = 2^d·s, s not a power of two): ||W'||_F^2 = 2^d ||W||_F^2 (M M^T = 2^d I)
+    and W' equals the dense product with the closed-form H_{n,d} = H_{2^d} ⊗ I_s."""
+    from oracle.transforms import hadamard_recursive
+    g = np.random.default_rng(4)
+    n, d = 1000, 3
+    W = g.standard_normal((23, n))
+    mult = synth.multiplier_abridged(5, n, d, n, "arht")
+    Wp = lra.preprocess_full(W, mult)
+    assert np.sum(Wp * Wp) == pytest.approx(8 * np.sum(W * W), rel=1e-13)
+    M = (mult["dsign"].astype(np.float64)[:, None] * hadamard_recursive(n, d))[:, mult["col"]]
+    assert np.allclose(Wp, W @ M, rtol=0, atol=1e-12 * np.abs(W).max())
+
+
+def test_alg101_backmap_residual_identity():
+    """Alg 10.1 with R = R_H H^+ = W[I,:]: the relative residual of the CUR LRA of W equals the
+    one computed on W' (M M^T = 2^d I); fp64 data so W' is exact."""
+    W = synth.factor_gaussian(8, 300, 256, 5, 1e-12)
+    mult = synth.multiplier_abridged(8, 256, 3, 256, "arht")
+    I0 = synth.random_rows(8, 300, 5)
+    res, rho_w = lra.cur_preprocessed(W, mult, 5, 5, 3, I0)
+    assert rho_w == pytest.approx(res.rho, rel=1e-9)
+    assert res.rho < 1e-5
