@@ -131,6 +131,17 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W /* host struct */,
                           const lra_multiplier *M /* host struct */, void *Y, int64_t ldy,
                           void *stream);
 
+/* Alg 10.1 stage 1 with u = n (the Table tb_fh protocol, with the
+   ARHT multiplier of P:6110-6124): Wout = W D H_{n,d} P, all n columns, m x n column-major in
+   W's dtype (ldo >= m).  M: kind ARHT, lbar == n, col = the whole permutation P (column c of
+   Wout = column col[c] of W D H_{n,d}), depth <= 5.  Each output is the fp64 signed sum over
+   its 2^d nonzeros in ascending t, rounded once to W's precision (reading C25).  Reads W once
+   and writes Wout once.  Then C-A and the nucleus run on Wout (I0 = a random start, Tests 2),
+   C = Wout[:,J], U = Wout_{k,l,r}^+ and R = R_H H^+ = W[I,:] (the residual of CUR on W equals
+   the one on Wout since M M^T = 2^d I).  Errors: EINVAL / EUNSUPPORTED synchronously. */
+lra_status lra_preprocess_full(lra_handle h, const lra_operand *W /* host struct */,
+                               const lra_multiplier *M /* host struct */, void *Wout, int64_t ldo, void *stream);
+
 /* Row-sharded operands (W.m_global > 0): the sketch Y is this rank's m x lbar part; every C-A
    block (Y, W[I,:]^T, W[:,J], W[I,J]) is assembled on every rank by an exact NCCL sum of the
    owners' rows and the maxvol runs replicated, so I, J, U, B are identical on every rank and

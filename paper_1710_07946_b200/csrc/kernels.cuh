@@ -47,6 +47,8 @@ struct SketchArgs {
   int64_t y_stride;                 // batch stride of Y (elements of double / double2)
 };
 cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st, Prof *pf);
+// NEXT-1: all n columns of W D H_{n,d} P (pinv: n ints of scratch)
+cudaError_t launch_transform_full(const SketchArgs &a, int *pinv, void *out, int64_t ldo, cudaStream_t st, Prof *pf);
 
 struct CAArgs {
   OpView op;

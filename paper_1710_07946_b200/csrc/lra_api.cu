@@ -368,6 +368,24 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multipli
   return LRA_OK;
 }
 
+lra_status lra_preprocess_full(lra_handle h, const lra_operand *W, const lra_multiplier *M, void *Wout, int64_t ldo,
+                               void *stream) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  if ((s = check_operand(W)) != LRA_OK) return s;
+  if (W->kind != LRA_OP_DENSE || W->m_global > 0) return fail(LRA_EINVAL, "lra_preprocess_full needs an unsharded dense operand");
+  if ((s = check_mult(M, W->n)) != LRA_OK) return s;
+  if (M->kind != LRA_MUL_ARHT) return fail(LRA_EUNSUPPORTED, "full pre-processing is implemented for ARHT");
+  if (M->lbar != W->n) return fail(LRA_EINVAL, "full pre-processing needs lbar == n (col = the whole permutation P)");
+  if (M->depth > 5) return fail(LRA_EUNSUPPORTED, "full pre-processing supports depth <= 5");
+  if (!Wout || ldo < W->m) return fail(LRA_EINVAL, "Wout null or ldo < m");
+  if ((s = ws_reserve(h, (size_t)W->n * sizeof(int) + 256)) != LRA_OK) return s;
+  SketchArgs a = make_sketch(W, M, Wout, ldo);
+  CK(launch_transform_full(a, (int *)h->ws, Wout, ldo, (cudaStream_t)stream, &h->prof));
+  h->launches += 2;
+  return LRA_OK;
+}
+
 static lra_status check_ca_shape(const lra_operand *W, int64_t r, int64_t k, int64_t l, int32_t sweeps) {
   if (k != l) return fail(LRA_EINVAL, "v1 requires k == l (reading C9)");
   if (r < 1 || r > k) return fail(LRA_EINVAL, "need 0 < r <= k");

@@ -212,6 +212,74 @@ __global__ void __launch_bounds__(128) k_sketch_gauss(SketchArgs a, const double
   (void)s_exact;
 }
 
+// ---------------------------------------------------------------- NEXT-1: all n columns
+// W' = W D H_{n,d} P (Alg 10.1 stage 1 with u = n, the Table tb_fh protocol): for fiber f the
+// 2^d columns k_t = f + t s of W feed the 2^d outputs sigma_u = f + u s, stored at column
+// c_u = P^{-1}(sigma_u):  W'[:, c_u] = sum_t (D[k_t] (-1)^popcount(t & u)) W[:, k_t]  in the
+// oracle's order (ascending t, fp64, one rounding to W's precision at the end, reading C25).
+// Each fiber's columns are read once and its outputs written once: 2 m n s_e bytes (HBM).
+// grid (ceil(m / 256), s), one row per thread.
+__global__ void k_perm_inverse(const int64_t *perm, int64_t n, int *pinv) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    pinv[perm[c]] = (int)c;
+}
+
+template <typename TW, int D>
+__global__ void __launch_bounds__(256) k_transform_full(const TW *W, int64_t m, int64_t n, int64_t ldw,
+                                                        const int8_t *dsign, const int *pinv, TW *Wp,
+                                                        int64_t ldo) {
+  constexpr int T = 1 << D;
+  const int64_t s = n >> D;
+  const int64_t f = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  __shared__ double s_d[T];
+  __shared__ int s_c[T];
+  if (threadIdx.x < T) {
+    s_d[threadIdx.x] = (double)dsign[f + threadIdx.x * s];
+    s_c[threadIdx.x] = pinv[f + threadIdx.x * s];
+  }
+  __syncthreads();
+  if (i >= m) return;
+  // D[k_t] W[i, k_t] (exact: D = +-1); with t and u unrolled the Hadamard sign is a constant,
+  // so each term is one fp64 add (products by +-1 are exact, the order is the oracle's)
+  double v[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) v[t] = s_d[t] * (double)__ldcs(W + (f + t * s) * ldw + i);
+#pragma unroll
+  for (int u = 0; u < T; ++u) {
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc = __dadd_rn(acc, ((__popc(t & u) & 1) ? -v[t] : v[t]));
+    __stcs(Wp + (int64_t)s_c[u] * ldo + i, (TW)acc);
+  }
+}
+
+template <typename TW>
+static cudaError_t launch_tf(const SketchArgs &a, const int *pinv, void *out, int64_t ldo, cudaStream_t st) {
+  dim3 grid((unsigned)((a.m + 255) / 256), (unsigned)(a.n >> a.depth));
+  const TW *W = reinterpret_cast<const TW *>(a.w);
+  TW *Wp = reinterpret_cast<TW *>(out);
+  switch (a.depth) {
+    case 1: k_transform_full<TW, 1><<<grid, 256, 0, st>>>(W, a.m, a.n, a.ldw, a.dsign, pinv, Wp, ldo); break;
+    case 2: k_transform_full<TW, 2><<<grid, 256, 0, st>>>(W, a.m, a.n, a.ldw, a.dsign, pinv, Wp, ldo); break;
+    case 3: k_transform_full<TW, 3><<<grid, 256, 0, st>>>(W, a.m, a.n, a.ldw, a.dsign, pinv, Wp, ldo); break;
+    case 4: k_transform_full<TW, 4><<<grid, 256, 0, st>>>(W, a.m, a.n, a.ldw, a.dsign, pinv, Wp, ldo); break;
+    case 5: k_transform_full<TW, 5><<<grid, 256, 0, st>>>(W, a.m, a.n, a.ldw, a.dsign, pinv, Wp, ldo); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transform_full(const SketchArgs &a, int *pinv, void *out, int64_t ldo, cudaStream_t st, Prof *pf) {
+  k_perm_inverse<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a.col, a.n, pinv);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  pf->begin("k_transform_full", st);
+  e = a.dtype == LRA_F32 ? launch_tf<float>(a, pinv, out, ldo, st) : launch_tf<double>(a, pinv, out, ldo, st);
+  pf->end(st);
+  return e;
+}
+
 cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo,
                           cudaStream_t st, Prof *pf) {
   if (a.kind == LRA_MUL_GAUSSIAN) {

@@ -74,6 +74,8 @@ def _load():
     lib.lra_batch.argtypes = [vp, i64, P(lra_operand), i64, P(lra_multiplier), i64, i64, i64, i64, i32, dbl, dbl,
                               i32, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.lra_last_error.restype = C.c_char_p
+    lib.lra_preprocess_full.argtypes = [vp, P(lra_operand), P(lra_multiplier), vp, i64, vp]
+    lib.lra_preprocess_full.restype = C.c_int
     lib.lra_nccl_unique_id.argtypes = [vp]
     lib.lra_nccl_unique_id.restype = C.c_int
     lib.lra_launch_count.argtypes = [vp]
@@ -103,7 +105,8 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id"]
+            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
+            "lra_preprocess_full"]
 
 
 def debug_counters(reset=True):
@@ -264,6 +267,12 @@ def lra_preprocess(h, W, M, Y, stream=None):
     """Y (lbar, m) float64 [or (lbar, m, 2) for ARFT] receives Y = W·M (column-major)."""
     ldy = Y.shape[1]
     _check(lib().lra_preprocess(h.h, C.byref(W.struct()), C.byref(M.struct()), _ptr(Y), ldy, _stream(stream)))
+
+
+def lra_preprocess_full(h, W, M, Wout, stream=None):
+    """Wout (n, m) tensor of W's dtype receives W' = W·D·H_{n,d}·P (Alg 10.1 stage 1, u = n)."""
+    _check(lib().lra_preprocess_full(h.h, C.byref(W.struct()), C.byref(M.struct()), _ptr(Wout), Wout.shape[-1],
+                                     _stream(stream)))
 
 
 def lra_cross_approx(h, W, Y, I0, r, k, l, sweeps, I, J, U, A, B, stats=None, y_complex=False,

@@ -60,3 +60,16 @@ def cur_batch(h, W, M, r, k, sweeps, nb, bufs=None, swap_tol=1e-12, tie_slack=1e
     L.lra_batch(h, nb, W, M, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2, bufs.stats,
                 swap_tol=swap_tol, tie_slack=tie_slack, stream=stream)
     return bufs
+
+
+def cur_preprocessed(h, W, M_full, r, k, sweeps, I0, stream=None):
+    """Alg 10.1 with C-A (the Table tb_fh protocol): W' = W·D·H_{n,d}·P (lra_preprocess_full),
+    then lra_cross_approx (random start I0) and lra_cur_residual on W'.  C = W'[:,J], U and
+    R = W[I,:] form the CUR LRA of W; the returned residual ratio (num2/den2 on W') equals the
+    one of W in exact arithmetic (M M^T = 2^d I).  Returns (bufs, Wp)."""
+    import torch
+    Wp = torch.empty_like(W.Wt)
+    L.lra_preprocess_full(h, W, M_full, Wp, stream=stream)
+    Wpd = L.Dense(Wp)
+    bufs = cur(h, Wpd, None, r, k, sweeps, I0=I0, stream=stream)
+    return bufs, Wp

@@ -405,3 +405,40 @@ def test_sharded_path_one_rank_matches_oracle(P, case):
     assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
     U = bufs.U.cpu().numpy().T
     assert np.allclose(U, ora.U, rtol=1e-9, atol=1e-9 * np.abs(ora.U).max())
+
+
+# ------------------------------------------------------------ NEXT-1: Alg 10.1 (tb_fh protocol)
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("m,n,d", [(1237, 1000, 3), (300, 96, 5), (4096, 4096, 4), (257, 64, 1)])
+def test_preprocess_full_bit_exact(P, h, dtype, m, n, d):
+    """W' = W D H_{n,d} P, all n columns (n = 2^d s with s not a power of two included):
+    bit-identical to the oracle (same ascending-t fp64 sums, one rounding)."""
+    W = np.asfortranarray(synth.factor_gaussian(m * 3 + n, m, n, 7, 1e-4).astype(dtype))
+    mult = synth.multiplier_abridged(9, n, d, n, "arht")
+    Wt = P.lra.to_colmajor(W)
+    Wp = torch.empty_like(Wt)
+    P.lra.lra_preprocess_full(h, P.lra.Dense(Wt), P.lra.Multiplier(mult), Wp)
+    torch.cuda.synchronize()
+    assert np.array_equal(Wp.cpu().numpy().T, O.preprocess_full(W, mult))
+
+
+def test_alg101_pipeline_vs_oracle(P, h):
+    """Alg 10.1 + C-A on BASELINE config-2 data (fp32 4096², ARHT d = 4 on all columns,
+    random I0, r = 32, k = l = 48, 3 loops): pivots bit-exact, rho on W' within 1e-4 of the
+    oracle's, which equals its rho on W with R = W[I,:] (back-map)."""
+    from paper_1710_07946_b200 import pipeline
+    W = synth.config2(0)
+    mult = synth.multiplier_abridged(0, 4096, 4, 4096, "arht")
+    I0 = synth.random_rows(0, 4096, 48)
+    ora, rho_w = O.cur_preprocessed(W, mult, 32, 48, 3, I0)
+    bufs, _ = pipeline.cur_preprocessed(h, _dense(P, W), P.lra.Multiplier(mult), 32, 48, 3,
+                                        torch.from_numpy(I0).cuda())
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)[0]
+    assert st["status"] == 0
+    assert list(bufs.I.cpu().numpy()) == list(ora.I) and list(bufs.J.cpu().numpy()) == list(ora.J)
+    rho = float(np.sqrt(bufs.num2.item() / bufs.den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4
+    # the back-mapped CUR of W (R = W[I,:]) has the same residual up to the fp32 rounding of W'
+    # (2^-24 per entry, ~10% of rho's per-entry size here)
+    assert abs(rho_w / ora.rho - 1) <= 1e-2
