@@ -71,7 +71,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
         self.t0 = self.t1 = None
@@ -85,15 +85,25 @@ class Clocks:
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = []
+        rows, all_rows = [], []
+        import datetime
         for line in open(self.f.name):
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                row = (float(parts[1]), float(parts[2]), parts[5:9])
             except ValueError:
                 continue
+            all_rows.append(row)
+            try:   # keep the samples taken inside the timed window
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if self.t0 is None or ts is None or (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
+                rows.append(row)
+        if not rows:
+            rows = all_rows
         os.unlink(self.f.name)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
@@ -177,7 +187,7 @@ def algorithmic(name, mult, B):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=28)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
@@ -235,6 +245,8 @@ def main():
     if ws > 1:
         dist.barrier()
     t1 = time.time()
+    if clocks:
+        clocks.window(t0, t1)
     ms = e0.elapsed_time(e1)
     launches = h.launches() - l0
     prof = h.profile_read()
