@@ -343,6 +343,31 @@ def sampled_residual(op, A, B, ii, jj):
     return op.m * op.n / Q * float(np.sum(d * d))
 
 
+def error_sample(op, A, B, rows, cols):
+    """Superfast a-posteriori estimation (Section spstr): the
+    q×s submatrix E[rows, cols] of E = W − CUR (CUR = A·B) gives K = q·s observed values g_i;
+    μ_K = (1/K) Σ g_i and σ_K² = (1/K) Σ |g_i − μ_K|² (reading C26: the paper's |g_i| in μ_K is
+    read as g_i, the sample mean of the variable whose variance is tested), and Σ g_i², which
+    extrapolates to ‖E‖_F² ≈ (mn/K) Σ g_i².  `op` is a DenseOperand or FactoredOperand."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    Wb = op.block(rows, cols)
+    Es = Wb - np.asarray(A, dtype=np.float64)[rows, :] @ np.asarray(B, dtype=np.float64)[:, cols]
+    g = Es.ravel()
+    K = g.size
+    mu = float(np.sum(g)) / K
+    var = float(np.sum((g - mu) ** 2)) / K
+    return mu, var, float(np.sum(g * g))
+
+
+def variance_upper_bound(var_K: float, K: int, alpha: float) -> float:
+    """One-sided (1−α) upper confidence bound on the variance σ² of a Gaussian variable from
+    the biased sample variance σ_K² of K observations (the customary chi-square rule the paper
+    refers to): K σ_K² / σ² ~ χ²_{K−1}, so σ² ≤ K σ_K² / χ²_{K−1}(α)."""
+    from scipy.stats import chi2
+    return K * var_K / chi2.ppf(alpha, K - 1)
+
+
 def factored_den2(op: FactoredOperand) -> float:
     """Exact ‖W‖_F² for W = A·B + E:  tr((AᵀA)(BBᵀ)) + 2·Σ_{(i,j)∈E} E_ij (A·B)_ij + Σ E_ij²."""
     G1 = op.A.T @ op.A

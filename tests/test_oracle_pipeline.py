@@ -209,3 +209,44 @@ def test_alg101_backmap_residual_identity():
     res, rho_w = lra.cur_preprocessed(W, mult, 5, 5, 3, I0)
     assert rho_w == pytest.approx(res.rho, rel=1e-9)
     assert res.rho < 1e-5
+
+
+# ------------------------------------------------------------ NEXT-2: superfast a-posteriori estimate
+def test_error_sample_full_grid_equals_residual():
+    """rows = all, cols = all: the sampled sum of squares is the full a-posteriori numerator."""
+    W = synth.factor_gaussian(11, 120, 90, 4, 1e-6)
+    mult = synth.multiplier_abridged(11, 90, 1, 4, "arht")
+    res = lra.cur_pipeline(W, mult, 4, 4, 4, 2)
+    mu, var, ss = lra.error_sample(lra.DenseOperand(W), res.A, res.B, np.arange(120), np.arange(90))
+    assert ss == pytest.approx(res.num2, rel=1e-12)
+    E = (W - res.A @ res.B).ravel()
+    assert mu == pytest.approx(E.mean(), rel=1e-9, abs=1e-18)          # numpy's own mean / var
+    assert var == pytest.approx(E.var(), rel=1e-9)
+
+
+def test_error_sample_recovers_known_noise_variance():
+    """W = A·B + E with E i.i.d. N(0, s²) and the exact factors: the q×s sample estimates s²
+    within its statistical error (sqrt(2/K) relative) and the chi-square bound covers it."""
+    g = np.random.default_rng(5)
+    m, n, r, sd = 2000, 1500, 6, 1e-3
+    A = g.standard_normal((m, r))
+    B = g.standard_normal((r, n))
+    W = A @ B + sd * g.standard_normal((m, n))
+    rows = g.choice(m, 100, replace=False)
+    cols = g.choice(n, 100, replace=False)
+    mu, var, _ = lra.error_sample(lra.DenseOperand(W), A, B, rows, cols)
+    assert abs(var / sd ** 2 - 1) < 5 * np.sqrt(2 / 1e4)
+    assert abs(mu) < 5 * sd / 100
+    assert lra.variance_upper_bound(var, 10000, 0.05) >= sd ** 2
+
+
+def test_variance_bound_coverage():
+    """Coverage of the one-sided 95 % chi-square bound over 400 independent samples of K = 200
+    standard normals (binomial 95 % ± 4.4 % at 4 sigma)."""
+    g = np.random.default_rng(6)
+    hits = 0
+    for _ in range(400):
+        x = g.standard_normal(200)
+        v = float(np.sum((x - x.mean()) ** 2)) / 200
+        hits += lra.variance_upper_bound(v, 200, 0.05) >= 1.0
+    assert abs(hits / 400 - 0.95) < 0.045
