@@ -174,6 +174,19 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
                             int64_t r, int32_t prec, int64_t nsamples, const int64_t *si,
                             const int64_t *sj, double *num2, double *den2, void *stream);
 
+/* Superfast a-posteriori estimation (Section "spstr"; NEXT-2): the q x s
+   submatrix E[rows, cols] of E = W - A B (rows[q], cols[s]: device int64) gives K = q s values
+   g_i; stats3 (device, 3 doubles) = { mu_K = sum g_i / K, sigma_K^2 = sum (g_i - mu_K)^2 / K
+   (reading C26), sum g_i^2 } — the last extrapolates to ||E||_F^2 ~ (m n / K) sum g_i^2.
+   W: dense or the factored entry oracle.  O(K r) work: superfast for K = O((m+n) k l). */
+lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A, const double *B, int64_t r,
+                            const int64_t *rows, int64_t q, const int64_t *cols, int64_t s, double *stats3,
+                            void *stream);
+/* The customary chi-square rule for the variance of a Gaussian variable: the
+   one-sided (1 - alpha) upper confidence bound  K sigma_K^2 / chi2_{K-1}(alpha)  on sigma^2
+   (chi-square quantile by Wilson-Hilferty; host scalars, 0 < alpha < 0.5, K >= 2). */
+lra_status lra_variance_bound(double var_K, int64_t K, double alpha, double *bound /* host */);
+
 /* A batch of nb independent dense problems (config 3, FMM-style blocks): block b
    is W0 with w = W0.w + b*w_stride elements (w_stride >= ldw*n).  SPARSE_PM1 multipliers may
    differ per block: sp_row / sp_sign of block b start at b*m_stride entries; ARHT / ARFT /

@@ -135,6 +135,9 @@ size_t residual_tc_scratch(int64_t m, int64_t n, int r, int S, int64_t nb);
 int64_t residual_tc_partials(int64_t m, int64_t n);
 cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, double *num2, double *den2,
                                cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_error_sample(const OpView &op, const double *A, const double *B, int r, const int64_t *rows,
+                                int64_t q, const int64_t *cols, int64_t s, double *g, double *out3, cudaStream_t st,
+                                int *nlaunch, Prof *pf);
 cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,
                            const int64_t *sj, int64_t Q, double2 *partial, int nblk, double *num2,
                            double *den2, cudaStream_t st, int *nlaunch, Prof *pf);

@@ -781,6 +781,58 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   return LRA_OK;
 }
 
+lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A, const double *B, int64_t r,
+                            const int64_t *rows, int64_t q, const int64_t *cols, int64_t s, double *stats3,
+                            void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "the sampled estimate is not row-sharded");
+  if (!A || !B || !rows || !cols || !stats3 || r < 1 || q < 1 || s < 1) return fail(LRA_EINVAL, "bad arguments");
+  if ((st = ws_reserve(h, (size_t)q * s * sizeof(double) + 256)) != LRA_OK) return st;
+  int nl = 0;
+  CK(launch_error_sample(make_view(W), A, B, (int)r, rows, q, cols, s, (double *)h->ws, stats3,
+                         (cudaStream_t)stream, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+// inverse of the standard normal CDF (Acklam's rational approximation, |rel err| < 1.2e-9)
+static double norm_ppf(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  const double pl = 0.02425;
+  if (p < pl) {
+    const double q = sqrt(-2 * log(p));
+    return (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+           ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  }
+  if (p > 1 - pl) {
+    const double q = sqrt(-2 * log(1 - p));
+    return -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+           ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  }
+  const double q = p - 0.5, rr = q * q;
+  return (((((a[0] * rr + a[1]) * rr + a[2]) * rr + a[3]) * rr + a[4]) * rr + a[5]) * q /
+         (((((b[0] * rr + b[1]) * rr + b[2]) * rr + b[3]) * rr + b[4]) * rr + 1);
+}
+
+lra_status lra_variance_bound(double var_K, int64_t K, double alpha, double *bound) {
+  if (!bound || K < 2 || !(alpha > 0.0 && alpha < 0.5) || !(var_K >= 0.0)) return fail(LRA_EINVAL, "bad arguments");
+  // chi-square quantile chi2_{K-1}(alpha) by Wilson-Hilferty
+  const double nu = (double)(K - 1), z = norm_ppf(alpha);
+  const double t = 1.0 - 2.0 / (9.0 * nu) + z * sqrt(2.0 / (9.0 * nu));
+  const double q = nu * t * t * t;
+  *bound = (double)K * var_K / q;
+  return LRA_OK;
+}
+
 lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_stride, const lra_multiplier *M0,
                      int64_t m_stride, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
                      double tie_slack, int32_t swap_cap, int32_t prec, int64_t *I, int64_t *J, double *U,

@@ -278,6 +278,79 @@ __global__ void __launch_bounds__(256) k_fact_den(FactOp f, int64_t n, double2 *
   }
 }
 
+// ------------------------------------------------ NEXT-2: q x s error submatrix statistics
+// g[a * s + b] = W(rows[a], cols[b]) - A[rows[a], :] B[:, cols[b]]  (Section spstr)
+__global__ void __launch_bounds__(256) k_error_sample(OpView op, const double *A, const double *B, int r,
+                                                      const int64_t *rows, int64_t q, const int64_t *cols,
+                                                      int64_t s, double *g) {
+  const int64_t K = q * s;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < K; e += (int64_t)gridDim.x * 256) {
+    const int64_t i = rows[e / s], j = cols[e % s];
+    double ab = 0.0;
+    for (int t = 0; t < r; ++t) ab = fma(A[(int64_t)t * op.m + i], B[j * r + t], ab);
+    g[e] = op.at(i, j) - ab;
+  }
+}
+// one CTA: mu = sum g / K, var = sum (g - mu)^2 / K, sum g^2 (fixed order: deterministic)
+__global__ void __launch_bounds__(1024) k_error_stats(const double *g, int64_t K, double *out3) {
+  __shared__ double red[2][32];
+  __shared__ double s_mu;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t e = threadIdx.x; e < K; e += 1024) {
+    const double x = g[e];
+    s1 += x;
+    s2 = fma(x, x, s2);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s1;
+    red[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 32; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    s_mu = a / (double)K;
+    out3[0] = s_mu;
+    out3[2] = b;
+  }
+  __syncthreads();
+  const double mu = s_mu;
+  double v = 0.0;
+  for (int64_t e = threadIdx.x; e < K; e += 1024) {
+    const double x = g[e] - mu;
+    v = fma(x, x, v);
+  }
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < 32; ++w) a += red[0][w];
+    out3[1] = a / (double)K;
+  }
+}
+
+cudaError_t launch_error_sample(const OpView &op, const double *A, const double *B, int r, const int64_t *rows,
+                                int64_t q, const int64_t *cols, int64_t s, double *g, double *out3, cudaStream_t st,
+                                int *nlaunch, Prof *pf) {
+  const int64_t K = q * s;
+  const unsigned grid = (unsigned)((K + 255) / 256 < 1184 ? (K + 255) / 256 : 1184);
+  pf->begin("k_error_sample", st);
+  k_error_sample<<<grid, 256, 0, st>>>(op, A, B, r, rows, q, cols, s, g);
+  pf->end(st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_error_stats<<<1, 1024, 0, st>>>(g, K, out3);
+  *nlaunch += 2;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,
                            const int64_t *sj, int64_t Q, double2 *partial, int nblk, double *num2,
                            double *den2, cudaStream_t st, int *nlaunch, Prof *pf) {

@@ -76,6 +76,10 @@ def _load():
     lib.lra_last_error.restype = C.c_char_p
     lib.lra_preprocess_full.argtypes = [vp, P(lra_operand), P(lra_multiplier), vp, i64, vp]
     lib.lra_preprocess_full.restype = C.c_int
+    lib.lra_error_sample.argtypes = [vp, P(lra_operand), vp, vp, i64, vp, i64, vp, i64, vp, vp]
+    lib.lra_error_sample.restype = C.c_int
+    lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
+    lib.lra_variance_bound.restype = C.c_int
     lib.lra_nccl_unique_id.argtypes = [vp]
     lib.lra_nccl_unique_id.restype = C.c_int
     lib.lra_launch_count.argtypes = [vp]
@@ -106,7 +110,7 @@ def lib():
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
-            "lra_preprocess_full"]
+            "lra_preprocess_full", "lra_error_sample", "lra_variance_bound"]
 
 
 def debug_counters(reset=True):
@@ -287,6 +291,18 @@ def lra_cross_approx(h, W, Y, I0, r, k, l, sweeps, I, J, U, A, B, stats=None, y_
 def lra_cur_residual(h, W, A, B, r, num2, den2, nsamples=0, si=None, sj=None, prec=LRA_RECON_PRECISE, stream=None):
     _check(lib().lra_cur_residual(h.h, C.byref(W.struct()), _ptr(A), _ptr(B), r, prec, nsamples, _ptr(si), _ptr(sj),
                                   _ptr(num2), _ptr(den2), _stream(stream)))
+
+
+def lra_error_sample(h, W, A, B, r, rows, cols, stats3, stream=None):
+    """stats3 (3,) float64 device tensor <- (mu_K, sigma_K^2, sum g^2) of E[rows, cols]."""
+    _check(lib().lra_error_sample(h.h, C.byref(W.struct()), _ptr(A), _ptr(B), r, _ptr(rows), rows.numel(),
+                                  _ptr(cols), cols.numel(), _ptr(stats3), _stream(stream)))
+
+
+def lra_variance_bound(var_K, K, alpha):
+    out = C.c_double()
+    _check(lib().lra_variance_bound(float(var_K), int(K), float(alpha), C.byref(out)))
+    return out.value
 
 
 def lra_batch(h, nb, W, M, r, k, l, sweeps, I, J, U, num2, den2, stats=None, swap_tol=1e-12, tie_slack=1e-12,

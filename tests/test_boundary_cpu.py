@@ -89,3 +89,14 @@ def test_product_path_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", txt, re.M), f
+
+
+def test_variance_bound_matches_chi_square(L):
+    """lra_variance_bound (host C, Wilson-Hilferty) vs scipy's exact chi-square quantile."""
+    from scipy.stats import chi2
+    for K in (100, 1000, 10000, 1000000):
+        for alpha in (0.01, 0.05, 0.2):
+            ref = K * 2.5e-7 / chi2.ppf(alpha, K - 1)
+            assert L.lra_variance_bound(2.5e-7, K, alpha) == pytest.approx(ref, rel=2e-3 if K == 100 else 2e-4)
+    with pytest.raises(L.LraError):
+        L.lra_variance_bound(1.0, 1, 0.05)

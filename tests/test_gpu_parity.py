@@ -442,3 +442,48 @@ def test_alg101_pipeline_vs_oracle(P, h):
     # the back-mapped CUR of W (R = W[I,:]) has the same residual up to the fp32 rounding of W'
     # (2^-24 per entry, ~10% of rho's per-entry size here)
     assert abs(rho_w / ora.rho - 1) <= 1e-2
+
+
+# ------------------------------------------------------------ NEXT-2: superfast a-posteriori estimate
+def test_error_sample_dense_vs_oracle(P, h):
+    """q x s sampled error statistics of the config-2 CUR (fp32 4096², the oracle's A, B): mean,
+    variance and sum of squares equal the oracle's to 1e-10 (summation order only)."""
+    W = synth.config2(1)
+    M = synth.multiplier_abridged(1, 4096, 4, 48, "arht")
+    ora = O.cur_pipeline(W, M, 32, 48, 48, 3, residual=False)
+    g = np.random.default_rng(2)
+    rows, cols = np.sort(g.choice(4096, 300, replace=False)), np.sort(g.choice(4096, 200, replace=False))
+    mu, var, ss = O.error_sample(O.DenseOperand(W), ora.A, ora.B, rows, cols)
+    At = torch.from_numpy(np.ascontiguousarray(ora.A.T)).cuda()
+    Bt = torch.from_numpy(np.ascontiguousarray(ora.B.T)).cuda()
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    P.lra.lra_error_sample(h, _dense(P, W), At, Bt, 32, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(), out)
+    torch.cuda.synchronize()
+    gm, gv, gs = out.cpu().numpy()
+    assert gv == pytest.approx(var, rel=1e-10) and gs == pytest.approx(ss, rel=1e-10)
+    assert abs(gm - mu) <= 1e-10 * np.sqrt(var) + 1e-300
+    # the superfast estimate brackets the full residual: sqrt(mn/K sum g^2) vs the exact numerator
+    num2, den2 = O.cur_residual(W, ora.A, ora.B)
+    est = 4096 * 4096 / (300 * 200) * gs
+    assert 0.5 < est / num2 < 2.0
+
+
+def test_error_sample_factored_entry_oracle(P, h):
+    """The same statistics on the config-4 entry oracle (W = A_W B_W + E never formed)."""
+    c4 = synth.config4(0, m=8192, n=8192, p=16, dens_ab=0.05, dens_e=1e-3)
+    op_o = O.FactoredOperand(c4["A"], c4["B"], c4["row_ptr"], c4["col"], c4["val"])
+    I0 = synth.random_rows(0, c4["m"], 24)
+    ca = O.cross_approx(op_o, 24, 24, 3, I0=I0)
+    Uo, Sr, sr, Tr = O.canonical_nucleus(op_o.block(ca.I, ca.J), 16)
+    Ao, Bo = O.rank_r_factors(op_o.cols(ca.J), op_o.rows(ca.I), Sr, sr, Tr)
+    g = np.random.default_rng(3)
+    rows, cols = g.choice(8192, 150, replace=False), g.choice(8192, 150, replace=False)
+    mu, var, ss = O.error_sample(op_o, Ao, Bo, rows, cols)
+    Wf, keep = _factored(P, c4)
+    At = torch.from_numpy(np.ascontiguousarray(Ao.T)).cuda()
+    Bt = torch.from_numpy(np.ascontiguousarray(Bo.T)).cuda()
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    P.lra.lra_error_sample(h, Wf, At, Bt, 16, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(), out)
+    torch.cuda.synchronize()
+    gm, gv, gs = out.cpu().numpy()
+    assert gv == pytest.approx(var, rel=1e-9) and gs == pytest.approx(ss, rel=1e-9)
