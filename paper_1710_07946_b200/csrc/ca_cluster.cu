@@ -34,6 +34,7 @@ namespace lra {
 // 0 loads, 1 cold LU, 2 warm gather + Newton, 3 Gauss-Jordan, 4 product, 5 swap loops,
 // 6 whole kernel, 7 pivot steps (count), 8 exact second rounds (count)
 __device__ unsigned long long g_cc_cyc[16];
+#define CC_MARK(kk) do { if (threadIdx.x == 0 && k.rank == 0) { long long _n = clock64(); atomicAdd(&g_cc_cyc[kk], (unsigned long long)(_n - _tm)); _tm = _n; } } while (0)
 
 namespace ccl {
 
@@ -110,6 +111,7 @@ struct Dec {
 template <int Q, class First, class Pub>
 __device__ __forceinline__ Dec pick(Kx<Q> &k, double mloc, First first, Pub publish, int &p) {
   Sh<Q> &sh = *k.sh;
+  long long _tm = clock64();
   p = k.par;
   k.par ^= 1;
   const unsigned long long wk = wmaxk(dkey(mloc));
@@ -132,9 +134,11 @@ __device__ __forceinline__ Dec pick(Kx<Q> &k, double mloc, First first, Pub publ
   const bool Camb = __any_sync(0xffffffffu, ck != Ck && ck != 0ull && kdbl(ck) >= Cthr);
   publish(p, Cidx);
   Dec d;
+  CC_MARK(9);
   if (k.cs > 1) {
     if (k.warp == 0 && k.lane < k.cs) *rmap(&sh.xin[p][k.rank], k.lane) = Trip{Ck, Cidx, Camb ? 1u : 0u};
     cluster_sync_all();
+    CC_MARK(10);
     const bool in = k.lane < k.cs;
     const Trip t = in ? sh.xin[p][k.lane] : Trip{0ull, 0xffffffffu, 0u};
     const unsigned long long Gk = wmaxk(t.key);
@@ -145,6 +149,7 @@ __device__ __forceinline__ Dec pick(Kx<Q> &k, double mloc, First first, Pub publ
     const unsigned bal = __ballot_sync(0xffffffffu, top && t.idx == d.idx);
     d.owner = bal ? __ffs(bal) - 1 : 0;
     d.M = kdbl(Gk);
+    CC_MARK(11);
   } else {
     __syncthreads();
     d.M = kdbl(Ck);
@@ -190,6 +195,7 @@ __device__ __forceinline__ Dec pick_exact(Kx<Q> &k, double mloc, double M, First
 // warp 0 copies the winning row (owner CTA's pub[p]) into prow and prepares pm / rc.
 template <int Q, class Prep>
 __device__ __forceinline__ void take_row(Kx<Q> &k, const Dec &d, int p, int q, Prep prep) {
+  long long _tm = clock64();
   if (k.warp == 0) {
     const double *src = k.cs > 1 ? rmap(&k.sh->pub[p][0], d.owner) : &k.sh->pub[p][0];
     double x[(Q + 31) / 32];
@@ -208,6 +214,7 @@ __device__ __forceinline__ void take_row(Kx<Q> &k, const Dec &d, int p, int q, P
     }
   }
   __syncthreads();
+  CC_MARK(12);
 }
 
 template <int OPK>
@@ -605,6 +612,7 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
           sh.pm[j] = (j == jstar) ? xv - 1.0 : xv;
           if (j == jstar) sh.rc = 1.0 / xv;
         });
+        long long _tm = clock64();
         if (threadIdx.x == 0) S[jstar] = istar;
         if (has && myslot == jstar) {                    // leaves S: explicit row e_{j*}
           myslot = -1;
@@ -641,6 +649,7 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
             }
           }
         }
+        CC_MARK(13);
         ++nsw;
       }
       if (threadIdx.x == 0 && k.rank == 0) atomicAdd(&g_cc_cyc[7], (unsigned long long)(nsw + (cold ? q : 0)));

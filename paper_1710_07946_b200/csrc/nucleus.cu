@@ -175,72 +175,84 @@ size_t nucleus_smem(int k, int l) {
 
 // ---------------------------------------------------------------------- factors
 
-// A = W[:,J] * TS.  grid (ceil(m/64), nb), 256 threads = 64 rows x 4 chunks of 16 outputs
-__global__ void __launch_bounds__(256) k_factor_A(FacArgs a) {
-  extern __shared__ double ts[];          // l x r
+// A = W[:,J] * TS: one thread per row of A computes all r outputs (accumulated in ascending j,
+// as before), the l gathered values W[i, J[j]] loaded 16 at a time (coalesced across rows).
+// grid (ceil(m/128), nb), 128 threads.  r <= 64 (registers: r doubles per thread).
+template <int RMAX>
+__global__ void __launch_bounds__(128) k_factor_A(FacArgs a) {
+  extern __shared__ double ts[];          // l x r: ts[t * l + j]
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int l = a.l, r = a.r;
   const double *TS = a.TS + b * (int64_t)l * r;
-  for (int e = threadIdx.x; e < l * r; e += 256) ts[e] = TS[e];   // ts[t*l + j]
+  for (int e = threadIdx.x; e < l * r; e += 128) ts[e] = TS[e];
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * 64 + (threadIdx.x & 63);
-  const int chunk = threadIdx.x >> 6;
-  if (i >= op.m || chunk * 16 >= r) return;
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (i >= op.m) return;
   const int64_t *J = a.J + b * l;
-  double acc[16];
+  double acc[RMAX];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
-  for (int j = 0; j < l; ++j) {
-    const double w = op.at(i, J[j]);
+  for (int u = 0; u < RMAX; ++u) acc[u] = 0.0;
+  for (int j0 = 0; j0 < l; j0 += 16) {
+    double w[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      int t = chunk * 16 + u;
-      if (t < r) acc[u] = fma(w, ts[t * l + j], acc[u]);
+    for (int x = 0; x < 16; ++x) w[x] = (j0 + x < l) ? op.at(i, J[j0 + x]) : 0.0;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      if (j0 + x < l) {
+#pragma unroll
+        for (int u = 0; u < RMAX; ++u)
+          if (u < r) acc[u] = fma(w[x], ts[u * l + j0 + x], acc[u]);
+      }
     }
   }
   double *A = a.A + b * a.a_stride;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    int t = chunk * 16 + u;
-    if (t < r) A[(int64_t)t * op.m + i] = acc[u];
-  }
+  for (int u = 0; u < RMAX; ++u)
+    if (u < r) A[(int64_t)u * op.m + i] = acc[u];
 }
 
-// B = Sr^T * W[I,:].  grid (ceil(n/64), nb), 256 threads = 64 columns x 4 chunks
-__global__ void __launch_bounds__(256) k_factor_B(FacArgs a) {
-  extern __shared__ double sr[];          // k x r
+// B = Sr^T * W[I,:]: one thread per column of B (all r outputs, ascending s), the k row
+// entries W[I[s], j] loaded 16 at a time.  grid (ceil(n/128), nb), 128 threads.
+template <int RMAX>
+__global__ void __launch_bounds__(128) k_factor_B(FacArgs a) {
+  extern __shared__ double sr[];          // k x r: sr[t * k + s]
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int k = a.k, r = a.r;
   const double *Sr = a.Sr + b * (int64_t)k * r;
-  for (int e = threadIdx.x; e < k * r; e += 256) sr[e] = Sr[e];   // sr[t*k + s]
+  for (int e = threadIdx.x; e < k * r; e += 128) sr[e] = Sr[e];
   __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * 64 + (threadIdx.x & 63);
-  const int chunk = threadIdx.x >> 6;
-  if (j >= op.n || chunk * 16 >= r) return;
+  const int64_t j = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (j >= op.n) return;
   const int64_t *I = a.I + b * k;
-  double acc[16];
+  double acc[RMAX];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
-  for (int s = 0; s < k; ++s) {
-    const double w = a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j);
+  for (int u = 0; u < RMAX; ++u) acc[u] = 0.0;
+  for (int s0 = 0; s0 < k; s0 += 16) {
+    double w[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      int t = chunk * 16 + u;
-      if (t < r) acc[u] = fma(sr[t * k + s], w, acc[u]);
+    for (int x = 0; x < 16; ++x) {
+      const int s = s0 + x;
+      w[x] = s < k ? (a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j)) : 0.0;
+    }
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      if (s0 + x < k) {
+#pragma unroll
+        for (int u = 0; u < RMAX; ++u)
+          if (u < r) acc[u] = fma(sr[u * k + s0 + x], w[x], acc[u]);
+      }
     }
   }
   double *B = a.B + b * a.b_stride;
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    int t = chunk * 16 + u;
-    if (t < r) B[j * r + t] = acc[u];
-  }
+  for (int u = 0; u < RMAX; ++u)
+    if (u < r) B[j * r + u] = acc[u];
 }
 
 cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf) {
@@ -254,17 +266,19 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   k_nucleus<<<(unsigned)nb, nt, smem, st>>>(na);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  dim3 gA((unsigned)((fa.op.m + 63) / 64), (unsigned)nb);
+  dim3 gA((unsigned)((fa.op.m + 127) / 128), (unsigned)nb);
   const size_t sA = (size_t)fa.l * fa.r * 8, sB = (size_t)fa.k * fa.r * 8;
-  if ((e = cudaFuncSetAttribute(k_factor_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sA)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_factor_B, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sB)) != cudaSuccess) return e;
+  void (*kA)(FacArgs) = fa.r <= 16 ? k_factor_A<16> : (fa.r <= 32 ? k_factor_A<32> : k_factor_A<64>);
+  void (*kB)(FacArgs) = fa.r <= 16 ? k_factor_B<16> : (fa.r <= 32 ? k_factor_B<32> : k_factor_B<64>);
+  if ((e = cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sA)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sB)) != cudaSuccess) return e;
   pf->begin("k_factor_A", st);
-  k_factor_A<<<gA, 256, sA, st>>>(fa);
+  kA<<<gA, 128, sA, st>>>(fa);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  dim3 gB((unsigned)((fa.op.n + 63) / 64), (unsigned)nb);
+  dim3 gB((unsigned)((fa.op.n + 127) / 128), (unsigned)nb);
   pf->begin("k_factor_B", st);
-  k_factor_B<<<gB, 256, sB, st>>>(fa);
+  kB<<<gB, 128, sB, st>>>(fa);
   pf->end(st);
   *nlaunch += 3;
   return cudaGetLastError();

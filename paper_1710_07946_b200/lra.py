@@ -117,7 +117,7 @@ def debug_counters(reset=True):
     out = (C.c_uint64 * 16)()
     _check(lib().lra_debug_counters(out, int(reset)))
     names = ["load", "cold_lu", "warm_gather", "gauss_jordan", "product", "swap_loop", "kernel", "pivot_steps",
-             "sw_ctamax", "sw_ctaidx", "sw_pub", "x_barrier", "x_triples", "x_prow", "sw_update", "-"]
+             "exact_rounds", "pk_reduce", "pk_cluster_bar", "pk_decide", "take_row", "sw_update", "-", "-"]
     return dict(zip(names, [int(x) for x in out]))
 
 
