@@ -176,12 +176,21 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
 
 /* Superfast a-posteriori estimation (Section "spstr"; NEXT-2): the q x s
    submatrix E[rows, cols] of E = W - A B (rows[q], cols[s]: device int64) gives K = q s values
-   g_i; stats3 (device, 3 doubles) = { mu_K = sum g_i / K, sigma_K^2 = sum (g_i - mu_K)^2 / K
-   (reading C26), sum g_i^2 } — the last extrapolates to ||E||_F^2 ~ (m n / K) sum g_i^2.
-   W: dense or the factored entry oracle.  O(K r) work: superfast for K = O((m+n) k l). */
+   g_i; stats3 (device, 4 doubles) = { mu_K = sum g_i / K, sigma_K^2 = sum (g_i - mu_K)^2 / K
+   (reading C26), sum g_i^2, sum W_ij^2 over the same entries } — the last two extrapolate to
+   ||E||_F^2 and ||W||_F^2 (times m n / K).  W: dense or the factored entry oracle.  O(K r)
+   work: superfast for K = O((m+n) k l). */
 lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A, const double *B, int64_t r,
                             const int64_t *rows, int64_t q, const int64_t *cols, int64_t s, double *stats3,
                             void *stream);
+/* A-priori error certificate of Corollary cowc1 (ii), eq. (eqnrm11), Frobenius
+   norm: |W - CUR| <= delta ((|R| + |C| + delta + eta |C||R||U|) xi |U| + 1), C = W[:,J],
+   R = W[I,:], U (l x k, device), eta = 1 if r = min(k,l) else 2, (1 - theta) xi = sqrt(k l),
+   theta = |U| eta delta with the spectral |U| bounded by |U|_F (reading C27); delta >= the
+   Frobenius tail sigma~_{r+1} of W (eq. eqnsgmrfr) is the caller's bound.  out4 (host) =
+   { bound (INFINITY when theta >= 1), |C|_F, |R|_F, |U|_F }.  Synchronizes the stream. */
+lra_status lra_cur_certificate(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, const double *U,
+                               int64_t k, int64_t l, int64_t r, double delta, double *out4 /* host */, void *stream);
 /* The customary chi-square rule for the variance of a Gaussian variable: the
    one-sided (1 - alpha) upper confidence bound  K sigma_K^2 / chi2_{K-1}(alpha)  on sigma^2
    (chi-square quantile by Wilson-Hilferty; host scalars, 0 < alpha < 0.5, K >= 2). */

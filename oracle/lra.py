@@ -348,7 +348,9 @@ def error_sample(op, A, B, rows, cols):
     q×s submatrix E[rows, cols] of E = W − CUR (CUR = A·B) gives K = q·s observed values g_i;
     μ_K = (1/K) Σ g_i and σ_K² = (1/K) Σ |g_i − μ_K|² (reading C26: the paper's |g_i| in μ_K is
     read as g_i, the sample mean of the variable whose variance is tested), and Σ g_i², which
-    extrapolates to ‖E‖_F² ≈ (mn/K) Σ g_i².  `op` is a DenseOperand or FactoredOperand."""
+    extrapolates to ‖E‖_F² ≈ (mn/K) Σ g_i², and Σ W_ij² over the same entries (the superfast
+    estimate of ‖W‖_F² used by the progressive mode).  `op` is a DenseOperand or
+    FactoredOperand."""
     rows = np.asarray(rows, dtype=np.int64)
     cols = np.asarray(cols, dtype=np.int64)
     Wb = op.block(rows, cols)
@@ -357,7 +359,7 @@ def error_sample(op, A, B, rows, cols):
     K = g.size
     mu = float(np.sum(g)) / K
     var = float(np.sum((g - mu) ** 2)) / K
-    return mu, var, float(np.sum(g * g))
+    return mu, var, float(np.sum(g * g)), float(np.sum(Wb * Wb))
 
 
 def variance_upper_bound(var_K: float, K: int, alpha: float) -> float:
@@ -366,6 +368,46 @@ def variance_upper_bound(var_K: float, K: int, alpha: float) -> float:
     refers to): K σ_K² / σ² ~ χ²_{K−1}, so σ² ≤ K σ_K² / χ²_{K−1}(α)."""
     from scipy.stats import chi2
     return K * var_K / chi2.ppf(alpha, K - 1)
+
+
+def cur_certificate(C, R, U, r: int, delta: float):
+    """A-priori error certificate of Corollary cowc1 (ii), eq. (eqnrm11), in
+    the Frobenius norm: |W − CUR| ≤ Δ·((|R| + |C| + Δ + μη|C||R||U|)·ξ|U| + 1) with μ = 1,
+    η = 1 if r = min(k, l) else 2, (1 − θ)ξ = √(kl), θ = ‖U‖ Δ_{k,l,r} ≤ ‖U‖ η Δ (Lemmas
+    leprtpsdinv, leprtinv), where Δ ≥ σ̃_{r+1} (eq. eqnsgmrfr) is the caller's bound.  ‖U‖ is
+    bounded by ‖U‖_F (reading C27).  Returns (bound or inf when θ ≥ 1, |C|_F, |R|_F, |U|_F)."""
+    C = np.asarray(C, dtype=np.float64)
+    R = np.asarray(R, dtype=np.float64)
+    U = np.asarray(U, dtype=np.float64)
+    l, k = U.shape
+    nc, nr, nu = float(np.linalg.norm(C)), float(np.linalg.norm(R)), float(np.linalg.norm(U))
+    eta = 1.0 if r == min(k, l) else 2.0
+    theta = nu * eta * delta
+    if theta >= 1.0:
+        return float("inf"), nc, nr, nu
+    xi = np.sqrt(k * l) / (1.0 - theta)
+    bound = delta * ((nr + nc + delta + eta * nc * nr * nu) * xi * nu + 1.0)
+    return float(bound), nc, nr, nu
+
+
+def cur_progressive(W, r: int, k: int, sweeps: int, tol: float, seed: int, rows, cols, dmax: int = 6):
+    """Progressive-depth pre-processing: for d = 1, 2, 3, … apply Alg 10.2 with
+    the ARHT multiplier of depth d (Philox seed `seed`) and accept the first CUR LRA whose
+    superfast estimate ((mn/K) Σ g²)/((mn/K) Σ W²) over the sampled rows × cols is ≤ tol²
+    (Section spstr).  Returns (d, CurResult, rho_estimate) (d = dmax result if none passes)."""
+    import synth
+    W = np.asarray(W)
+    m, n = W.shape
+    op = DenseOperand(W)
+    d = 1
+    while True:
+        mult = synth.multiplier_abridged(seed, n, d, k, "arht")
+        res = cur_pipeline(W, mult, r, k, k, sweeps, residual=False)
+        _, _, ss, sw = error_sample(op, res.A, res.B, rows, cols)
+        est = float(np.sqrt(ss / sw)) if sw > 0 else float("inf")
+        if est <= tol or d >= dmax or n % (1 << (d + 1)):
+            return d, res, est
+        d += 1
 
 
 def factored_den2(op: FactoredOperand) -> float:

@@ -789,11 +789,41 @@ lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A,
   if ((st = check_operand(W)) != LRA_OK) return st;
   if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "the sampled estimate is not row-sharded");
   if (!A || !B || !rows || !cols || !stats3 || r < 1 || q < 1 || s < 1) return fail(LRA_EINVAL, "bad arguments");
-  if ((st = ws_reserve(h, (size_t)q * s * sizeof(double) + 256)) != LRA_OK) return st;
+  if ((st = ws_reserve(h, (size_t)2 * q * s * sizeof(double) + 256)) != LRA_OK) return st;
   int nl = 0;
   CK(launch_error_sample(make_view(W), A, B, (int)r, rows, q, cols, s, (double *)h->ws, stats3,
                          (cudaStream_t)stream, &nl, &h->prof));
   h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_cur_certificate(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, const double *U,
+                               int64_t k, int64_t l, int64_t r, double delta, double *out4, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "the certificate is not row-sharded");
+  if (!I || !J || !U || !out4 || k < 1 || l < 1 || r < 1 || r > (k < l ? k : l) || !(delta >= 0.0))
+    return fail(LRA_EINVAL, "bad arguments");
+  if ((st = ws_reserve(h, 3 * sizeof(double) + 256)) != LRA_OK) return st;
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(launch_cert_norms(make_view(W), I, J, (int)k, (int)l, U, (double *)h->ws, sm));
+  double nn[3];
+  CK(cudaMemcpyAsync(nn, h->ws, sizeof(nn), cudaMemcpyDeviceToHost, sm));
+  CK(cudaStreamSynchronize(sm));
+  h->launches += 1;
+  const double nc = sqrt(nn[0]), nr = sqrt(nn[1]), nu = sqrt(nn[2]);
+  const double eta = (r == (k < l ? k : l)) ? 1.0 : 2.0;
+  const double theta = nu * eta * delta;       // ||U|| bounded by ||U||_F (reading C27)
+  double bound = INFINITY;
+  if (theta < 1.0) {
+    const double xi = sqrt((double)k * (double)l) / (1.0 - theta);
+    bound = delta * ((nr + nc + delta + eta * nc * nr * nu) * xi * nu + 1.0);
+  }
+  out4[0] = bound;
+  out4[1] = nc;
+  out4[2] = nr;
+  out4[3] = nu;
   return LRA_OK;
 }
 

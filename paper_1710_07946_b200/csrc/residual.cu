@@ -288,35 +288,42 @@ __global__ void __launch_bounds__(256) k_error_sample(OpView op, const double *A
     const int64_t i = rows[e / s], j = cols[e % s];
     double ab = 0.0;
     for (int t = 0; t < r; ++t) ab = fma(A[(int64_t)t * op.m + i], B[j * r + t], ab);
-    g[e] = op.at(i, j) - ab;
+    const double w = op.at(i, j);
+    g[e] = w - ab;
+    g[K + e] = w;        // the sampled entries of W (superfast estimate of ||W||_F^2)
   }
 }
-// one CTA: mu = sum g / K, var = sum (g - mu)^2 / K, sum g^2 (fixed order: deterministic)
+// one CTA: mu = sum g / K, var = sum (g - mu)^2 / K, sum g^2, sum W^2 (fixed order: deterministic)
 __global__ void __launch_bounds__(1024) k_error_stats(const double *g, int64_t K, double *out3) {
-  __shared__ double red[2][32];
+  __shared__ double red[3][32];
   __shared__ double s_mu;
-  double s1 = 0.0, s2 = 0.0;
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0;
   for (int64_t e = threadIdx.x; e < K; e += 1024) {
-    const double x = g[e];
+    const double x = g[e], w = g[K + e];
     s1 += x;
     s2 = fma(x, x, s2);
+    s3 = fma(w, w, s3);
   }
   s1 = warp_sum(s1);
   s2 = warp_sum(s2);
+  s3 = warp_sum(s3);
   if ((threadIdx.x & 31) == 0) {
     red[0][threadIdx.x >> 5] = s1;
     red[1][threadIdx.x >> 5] = s2;
+    red[2][threadIdx.x >> 5] = s3;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
+    double a = 0.0, b = 0.0, c = 0.0;
     for (int w = 0; w < 32; ++w) {
       a += red[0][w];
       b += red[1][w];
+      c += red[2][w];
     }
     s_mu = a / (double)K;
     out3[0] = s_mu;
     out3[2] = b;
+    out3[3] = c;
   }
   __syncthreads();
   const double mu = s_mu;
@@ -334,6 +341,43 @@ __global__ void __launch_bounds__(1024) k_error_stats(const double *g, int64_t K
     for (int w = 0; w < 32; ++w) a += red[0][w];
     out3[1] = a / (double)K;
   }
+}
+
+// ||W[:,J]||_F^2, ||W[I,:]||_F^2, ||U||_F^2 -> out3 (one CTA each, fixed order)
+__global__ void __launch_bounds__(1024) k_cert_norms(OpView op, const int64_t *I, const int64_t *J, int k, int l,
+                                                     const double *U, double *out3) {
+  __shared__ double red[32];
+  const int which = blockIdx.x;
+  double acc = 0.0;
+  if (which == 0) {
+    const int64_t tot = op.m * l;
+    for (int64_t e = threadIdx.x; e < tot; e += 1024) {
+      const double w = op.at(e % op.m, J[e / op.m]);
+      acc = fma(w, w, acc);
+    }
+  } else if (which == 1) {
+    const int64_t tot = (int64_t)k * op.n;
+    for (int64_t e = threadIdx.x; e < tot; e += 1024) {
+      const double w = op.at(I[e % k], e / k);
+      acc = fma(w, w, acc);
+    }
+  } else {
+    for (int64_t e = threadIdx.x; e < (int64_t)k * l; e += 1024) acc = fma(U[e], U[e], acc);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < 32; ++w) a += red[w];
+    out3[which] = a;
+  }
+}
+
+cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,
+                              double *out3, cudaStream_t st) {
+  k_cert_norms<<<3, 1024, 0, st>>>(op, I, J, k, l, U, out3);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_error_sample(const OpView &op, const double *A, const double *B, int r, const int64_t *rows,

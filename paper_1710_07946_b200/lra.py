@@ -78,6 +78,8 @@ def _load():
     lib.lra_preprocess_full.restype = C.c_int
     lib.lra_error_sample.argtypes = [vp, P(lra_operand), vp, vp, i64, vp, i64, vp, i64, vp, vp]
     lib.lra_error_sample.restype = C.c_int
+    lib.lra_cur_certificate.argtypes = [vp, P(lra_operand), vp, vp, vp, i64, i64, i64, dbl, P(C.c_double), vp]
+    lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
     lib.lra_nccl_unique_id.argtypes = [vp]
@@ -110,7 +112,8 @@ def lib():
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
-            "lra_preprocess_full", "lra_error_sample", "lra_variance_bound"]
+            "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
+            "lra_cur_certificate"]
 
 
 def debug_counters(reset=True):
@@ -293,8 +296,16 @@ def lra_cur_residual(h, W, A, B, r, num2, den2, nsamples=0, si=None, sj=None, pr
                                   _ptr(num2), _ptr(den2), _stream(stream)))
 
 
+def lra_cur_certificate(h, W, I, J, U, k, l, r, delta, stream=None):
+    """(bound, |C|_F, |R|_F, |U|_F) of Cor cowc1 for the Frobenius-tail bound delta."""
+    out = (C.c_double * 4)()
+    _check(lib().lra_cur_certificate(h.h, C.byref(W.struct()), _ptr(I), _ptr(J), _ptr(U), k, l, r, float(delta), out,
+                                     _stream(stream)))
+    return tuple(out)
+
+
 def lra_error_sample(h, W, A, B, r, rows, cols, stats3, stream=None):
-    """stats3 (3,) float64 device tensor <- (mu_K, sigma_K^2, sum g^2) of E[rows, cols]."""
+    """stats3 (4,) float64 device tensor <- (mu_K, sigma_K^2, sum g^2, sum W^2) of E[rows, cols]."""
     _check(lib().lra_error_sample(h.h, C.byref(W.struct()), _ptr(A), _ptr(B), r, _ptr(rows), rows.numel(),
                                   _ptr(cols), cols.numel(), _ptr(stats3), _stream(stream)))
 

@@ -73,3 +73,25 @@ def cur_preprocessed(h, W, M_full, r, k, sweeps, I0, stream=None):
     Wpd = L.Dense(Wp)
     bufs = cur(h, Wpd, None, r, k, sweeps, I0=I0, stream=stream)
     return bufs, Wp
+
+
+def cur_progressive(h, W, r, k, sweeps, tol, seed, rows, cols, dmax=6, stream=None):
+    """Progressive-depth pre-processing: d = 1, 2, 3, ... with the ARHT
+    multiplier of depth d (realized by the seeded generator) until the superfast sampled
+    estimate sqrt(sum g^2 / sum W^2) over rows x cols (lra_error_sample) is <= tol.
+    Returns (d, bufs, estimate)."""
+    import synth
+    stats = torch.empty(4, dtype=torch.float64, device=W.Wt.device)
+    d = 1
+    while True:
+        M = L.Multiplier(synth.multiplier_abridged(seed, W.n, d, k, "arht"))
+        bufs = CurBuffers(W.m, W.n, r, k)
+        L.lra_preprocess(h, W, M, bufs.Y, stream=stream)
+        L.lra_cross_approx(h, W, bufs.Y, None, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.A, bufs.B, bufs.stats,
+                           stream=stream)
+        L.lra_error_sample(h, W, bufs.A, bufs.B, r, rows, cols, stats, stream=stream)
+        _, _, ss, sw = stats.tolist()
+        est = (ss / sw) ** 0.5 if sw > 0 else float("inf")
+        if est <= tol or d >= dmax or W.n % (1 << (d + 1)):
+            return d, bufs, est
+        d += 1

@@ -453,14 +453,15 @@ def test_error_sample_dense_vs_oracle(P, h):
     ora = O.cur_pipeline(W, M, 32, 48, 48, 3, residual=False)
     g = np.random.default_rng(2)
     rows, cols = np.sort(g.choice(4096, 300, replace=False)), np.sort(g.choice(4096, 200, replace=False))
-    mu, var, ss = O.error_sample(O.DenseOperand(W), ora.A, ora.B, rows, cols)
+    mu, var, ss, sw = O.error_sample(O.DenseOperand(W), ora.A, ora.B, rows, cols)
     At = torch.from_numpy(np.ascontiguousarray(ora.A.T)).cuda()
     Bt = torch.from_numpy(np.ascontiguousarray(ora.B.T)).cuda()
-    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
     P.lra.lra_error_sample(h, _dense(P, W), At, Bt, 32, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(), out)
     torch.cuda.synchronize()
-    gm, gv, gs = out.cpu().numpy()
+    gm, gv, gs, gw = out.cpu().numpy()
     assert gv == pytest.approx(var, rel=1e-10) and gs == pytest.approx(ss, rel=1e-10)
+    assert gw == pytest.approx(sw, rel=1e-13)
     assert abs(gm - mu) <= 1e-10 * np.sqrt(var) + 1e-300
     # the superfast estimate brackets the full residual: sqrt(mn/K sum g^2) vs the exact numerator
     num2, den2 = O.cur_residual(W, ora.A, ora.B)
@@ -478,12 +479,42 @@ def test_error_sample_factored_entry_oracle(P, h):
     Ao, Bo = O.rank_r_factors(op_o.cols(ca.J), op_o.rows(ca.I), Sr, sr, Tr)
     g = np.random.default_rng(3)
     rows, cols = g.choice(8192, 150, replace=False), g.choice(8192, 150, replace=False)
-    mu, var, ss = O.error_sample(op_o, Ao, Bo, rows, cols)
+    mu, var, ss, sw = O.error_sample(op_o, Ao, Bo, rows, cols)
     Wf, keep = _factored(P, c4)
     At = torch.from_numpy(np.ascontiguousarray(Ao.T)).cuda()
     Bt = torch.from_numpy(np.ascontiguousarray(Bo.T)).cuda()
-    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
     P.lra.lra_error_sample(h, Wf, At, Bt, 16, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(), out)
     torch.cuda.synchronize()
-    gm, gv, gs = out.cpu().numpy()
+    gm, gv, gs, gw = out.cpu().numpy()
     assert gv == pytest.approx(var, rel=1e-9) and gs == pytest.approx(ss, rel=1e-9)
+
+
+def test_certificate_vs_oracle(P, h):
+    """Cor cowc1 certificate through the C-ABI equals the oracle's formula (norms to 1e-12)."""
+    W = synth.config2(0)
+    M = synth.multiplier_abridged(0, 4096, 4, 48, "arht")
+    ora = O.cur_pipeline(W, M, 32, 48, 48, 3, residual=False)
+    op = O.DenseOperand(W)
+    delta = 1e-6
+    ref = O.cur_certificate(op.cols(ora.J), op.rows(ora.I), ora.U, 32, delta)
+    I = torch.from_numpy(ora.I).cuda()
+    J = torch.from_numpy(ora.J).cuda()
+    U = torch.from_numpy(np.ascontiguousarray(ora.U.T)).cuda()
+    got = P.lra.lra_cur_certificate(h, _dense(P, W), I, J, U, 48, 48, 32, delta)
+    for a, b in zip(got, ref):
+        assert a == pytest.approx(b, rel=1e-12) or (np.isinf(a) and np.isinf(b))
+
+
+def test_progressive_depth_vs_oracle(P, h):
+    """Progressive-depth mode: same accepted depth and pivots as the oracle."""
+    from paper_1710_07946_b200 import pipeline
+    W = synth.factor_gaussian(3, 256, 256, 6, 1e-10)
+    g = np.random.default_rng(0)
+    rows, cols = g.choice(256, 40, replace=False), g.choice(256, 40, replace=False)
+    d_o, res_o, est_o = O.cur_progressive(W, 6, 8, 2, 1e-3, 1, rows, cols, dmax=4)
+    d, bufs, est = pipeline.cur_progressive(h, _dense(P, W), 6, 8, 2, 1e-3, 1, torch.from_numpy(rows).cuda(),
+                                            torch.from_numpy(cols).cuda(), dmax=4)
+    assert d == d_o
+    assert list(bufs.I.cpu().numpy()) == list(res_o.I) and list(bufs.J.cpu().numpy()) == list(res_o.J)
+    assert est == pytest.approx(est_o, rel=1e-6)

@@ -217,8 +217,9 @@ def test_error_sample_full_grid_equals_residual():
     W = synth.factor_gaussian(11, 120, 90, 4, 1e-6)
     mult = synth.multiplier_abridged(11, 90, 1, 4, "arht")
     res = lra.cur_pipeline(W, mult, 4, 4, 4, 2)
-    mu, var, ss = lra.error_sample(lra.DenseOperand(W), res.A, res.B, np.arange(120), np.arange(90))
+    mu, var, ss, sw = lra.error_sample(lra.DenseOperand(W), res.A, res.B, np.arange(120), np.arange(90))
     assert ss == pytest.approx(res.num2, rel=1e-12)
+    assert sw == pytest.approx(res.den2, rel=1e-13)
     E = (W - res.A @ res.B).ravel()
     assert mu == pytest.approx(E.mean(), rel=1e-9, abs=1e-18)          # numpy's own mean / var
     assert var == pytest.approx(E.var(), rel=1e-9)
@@ -234,7 +235,7 @@ def test_error_sample_recovers_known_noise_variance():
     W = A @ B + sd * g.standard_normal((m, n))
     rows = g.choice(m, 100, replace=False)
     cols = g.choice(n, 100, replace=False)
-    mu, var, _ = lra.error_sample(lra.DenseOperand(W), A, B, rows, cols)
+    mu, var, _, _ = lra.error_sample(lra.DenseOperand(W), A, B, rows, cols)
     assert abs(var / sd ** 2 - 1) < 5 * np.sqrt(2 / 1e4)
     assert abs(mu) < 5 * sd / 100
     assert lra.variance_upper_bound(var, 10000, 0.05) >= sd ** 2
@@ -250,3 +251,33 @@ def test_variance_bound_coverage():
         v = float(np.sum((x - x.mean()) ** 2)) / 200
         hits += lra.variance_upper_bound(v, 200, 0.05) >= 1.0
     assert abs(hits / 400 - 0.95) < 0.045
+
+
+def test_certificate_holds_and_vanishes():
+    """Cor cowc1 (ii): with Δ = σ̃_{r+1} (the Frobenius tail of W's spectrum, eq. eqnsgmrfr)
+    the certificate bounds ||W − CUR||_F on random perturbed low-rank inputs; for an exactly
+    rank-r W (Δ = 0) it is 0 and W = CUR (thm thcandec)."""
+    for seed in range(6):
+        W = synth.factor_gaussian(40 + seed, 200, 150, 5, 1e-8 * (seed + 1))
+        mult = synth.multiplier_abridged(seed, 150, 1, 7, "arht")
+        res = lra.cur_pipeline(W, mult, 5, 7, 7, 2)
+        sv = np.linalg.svd(W, compute_uv=False)
+        delta = float(np.sqrt(np.sum(sv[5:] ** 2)))
+        op = lra.DenseOperand(W)
+        bound, nc, nr, nu = lra.cur_certificate(op.cols(res.J), op.rows(res.I), res.U, 5, delta)
+        assert np.sqrt(res.num2) <= bound
+        assert nc == pytest.approx(np.linalg.norm(W[:, res.J])) and nu == pytest.approx(np.linalg.norm(res.U))
+    b0, *_ = lra.cur_certificate(np.ones((4, 2)), np.ones((2, 4)), np.eye(2), 2, 0.0)
+    assert b0 == 0.0
+
+
+def test_progressive_depth_stops_at_first_passing_depth():
+    """d = 1 already passes on a generic perturbed low-rank input; an impossible
+    tolerance runs to dmax; the estimate is the sampled ratio."""
+    W = synth.factor_gaussian(3, 256, 256, 6, 1e-10)
+    g = np.random.default_rng(0)
+    rows, cols = g.choice(256, 40, replace=False), g.choice(256, 40, replace=False)
+    d, res, est = lra.cur_progressive(W, 6, 8, 2, 1e-3, 1, rows, cols, dmax=4)
+    assert d == 1 and est <= 1e-3
+    d2, _, est2 = lra.cur_progressive(W, 6, 8, 2, 1e-30, 1, rows, cols, dmax=3)
+    assert d2 == 3 and est2 > 1e-30
