@@ -518,3 +518,71 @@ def test_progressive_depth_vs_oracle(P, h):
     assert d == d_o
     assert list(bufs.I.cpu().numpy()) == list(res_o.I) and list(bufs.J.cpu().numpy()) == list(res_o.J)
     assert est == pytest.approx(est_o, rel=1e-6)
+
+
+# ------------------------------------------------------------ strided operands, fp64 FAST, config 5 full size
+def _dense_padded(P, W, pad):
+    """W (m x n) stored column-major with leading dimension m + pad (a view of a larger array)."""
+    m, n = W.shape
+    big = torch.zeros((n, m + pad), dtype=torch.float32 if W.dtype == np.float32 else torch.float64, device="cuda")
+    big[:, :m] = torch.from_numpy(np.ascontiguousarray(W.T)).cuda()
+    op = P.lra.Dense(big)
+    st = op.struct
+    op.struct = lambda: _with_m(st, m, m + pad)   # m = logical rows, ldw = m + pad (storage)
+    op.m = m
+    return op, big
+
+
+def _with_m(st, m, ldw):
+    s = st()
+    s.m = m
+    s.ldw = ldw
+    return s
+
+
+@pytest.mark.parametrize("pad", [1, 3, 5])
+def test_leading_dimension_padding(P, h, pad):
+    """ldw > m (odd padding breaks 16-byte alignment of the columns): sketch, C-A, nucleus and
+    the tensor-core residual agree with the oracle on the unpadded matrix."""
+    from paper_1710_07946_b200 import pipeline
+    m, n, k, r = 700, 512, 16, 12
+    W = synth.factor_gaussian(77, m, n, r, 1e-9).astype(np.float32)
+    M = synth.multiplier_abridged(7, n, 3, k, "arht")
+    ora = O.cur_pipeline(W, M, r, k, k, 3)
+    op, keep = _dense_padded(P, W, pad)
+    bufs = pipeline.cur(h, op, P.lra.Multiplier(M), r, k, 3)
+    torch.cuda.synchronize()
+    assert list(bufs.I.cpu().numpy()) == list(ora.I) and list(bufs.J.cpu().numpy()) == list(ora.J)
+    rho = float(np.sqrt(bufs.num2.item() / bufs.den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4
+    assert bufs.den2.item() == pytest.approx(ora.den2, rel=1e-13)
+
+
+def test_residual_tc_fast_fp64(P, h):
+    """FAST mode on fp64 W (tensor-core path with double W tiles)."""
+    g = np.random.default_rng(15)
+    m, n, r = 1500, 1100, 24
+    A = g.standard_normal((m, r)) / 4
+    B = g.standard_normal((r, n)) / 4
+    W = A @ B + 0.05 * g.standard_normal((m, n))
+    num_o, den_o = O.cur_residual(W, A, B)
+    num2, den2 = _residual_gpu(P, h, np.asfortranarray(W), A, B, r, P.lra.LRA_RECON_FAST)
+    assert num2 == pytest.approx(num_o, rel=1e-4)
+    assert den2 == pytest.approx(den_o, rel=1e-13)
+
+
+@pytest.mark.slow
+def test_config5_full_size_invariants():
+    """BASELINE config 5 at full size (131072², 68.7 GB fp32) on one GPU through the C-ABI:
+    status OK, dominance certificates <= 1 + 1e-12 on both sides, sampled sketch rows
+    bit-exact against an fp64 recomputation from the same bits (tools/config5_run.py)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "tools/config5_run.py"], cwd=root, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    out = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["status"] == 0 and out["sketch_rows_exact"]
+    assert out["cert_rows"] <= 1 + 1e-12 and out["cert_cols"] <= 1 + 1e-12
