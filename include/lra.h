@@ -174,6 +174,19 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
                             int64_t r, int32_t prec, int64_t nsamples, const int64_t *si,
                             const int64_t *sj, double *num2, double *den2, void *stream);
 
+/* Rectangular generators (NEXT-3): greedy expansion of the column set J[0..g0) of the k x g0
+   submatrix W[I, J] to l >= g0 columns (Alg D.4 "algrup"): each appended column j
+   maximizes v2^2 growth 1 + b_j^T (C C^T)^{-1} b_j (eq. eqbun), ties -> smallest j among
+   scores >= (1 - tie_slack) max (reading C11).  J (device, l entries) holds the g0 start
+   columns on entry and all l on return.  Requires k <= g0 (C full row rank), k <= 128. */
+lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t g0,
+                              int64_t l, double tie_slack, void *stream);
+/* Canonical nucleus U = W_{k,l,r}^+ (Alg 3.1) of the generator W[I,J] (any k x l,
+   k, l <= 128) and the factors A = W[:,J] T_r Sigma_r^{-1} (m x r), B = S_r^T W[I,:] (r x n),
+   as lra_cross_approx computes them for k = l.  status (device int32): LRA_OK or ESINGULAR. */
+lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, int64_t k,
+                               int64_t l, int64_t r, double *U, double *A, double *B, int32_t *status, void *stream);
+
 /* Superfast a-posteriori estimation (Section "spstr"; NEXT-2): the q x s
    submatrix E[rows, cols] of E = W - A B (rows[q], cols[s]: device int64) gives K = q s values
    g_i; stats3 (device, 4 doubles) = { mu_K = sum g_i / K, sigma_K^2 = sum (g_i - mu_K)^2 / K

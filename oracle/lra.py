@@ -296,6 +296,47 @@ def cross_approx(op, k: int, l: int, sweeps: int, Y=None, I0=None, J0=None,
     return CAResult(I, J, loops, lu, sw, ch, cert_r, cert_c, logdet_steps, steps)
 
 
+# ============================================ rectangular generators (Alg D.4, NEXT-3)
+def expand_columns(R: np.ndarray, J, l: int, tau: float = TAU):
+    """Greedy expansion of the k×g submatrix C_g = R[:, J] of the k×n matrix R (g ≥ k, full
+    row rank) to k×l (Alg D.4 "algrup"): the column b appended at each step
+    maximizes v₂(C_g | b)² = v₂(C_g)²·(1 + bᵀ(C_g C_gᵀ)⁻¹ b) (eq. eqbun), i.e. the score
+    ‖L⁻¹ b‖² with L Lᵀ = C_g C_gᵀ (Cholesky, then forward substitution — the "orthogonalizing
+    pre-multiplication R_g" of stage 1 is L⁻¹).  Ties: smallest column among scores ≥
+    (1 − τ)·max (reading C11).  Returns (J extended to l columns, list of scores)."""
+    import scipy.linalg
+    R = np.asarray(R, dtype=np.float64)
+    J = [int(j) for j in J]
+    scores = []
+    n = R.shape[1]
+    while len(J) < l:
+        C = R[:, J]
+        L = np.linalg.cholesky(C @ C.T)
+        Z = scipy.linalg.solve_triangular(L, R, lower=True)
+        sc = np.sum(Z * Z, axis=0)
+        sc[J] = -1.0
+        mx = float(sc.max())
+        j = int(np.flatnonzero(sc >= (1.0 - tau) * mx)[0])
+        J.append(j)
+        scores.append(mx)
+    return np.array(J, dtype=np.int64), scores
+
+
+def cur_rectangular(W, mult, r: int, k: int, l: int, sweeps: int, I0=None) -> "CurResult":
+    """k×l generators with l > k (NEXT-3): the square C-A of Alg 10.2 (k = k) gives (I, J),
+    Alg D.4 expands J greedily to l columns on R = W[I,:], then the canonical nucleus
+    U = W_{k,l,r}^+ (Alg 3.1, rectangular) and CUR = A·B with A = W[:,J] T_r Σ_r⁻¹,
+    B = S_rᵀ W[I,:]."""
+    op = DenseOperand(W)
+    Y = sketch(W, mult) if mult is not None else None
+    ca = cross_approx(op, k, k, sweeps, Y=Y, I0=I0)
+    J, _ = expand_columns(op.rows(ca.I), ca.J, l)
+    U, Sr, sr, Tr = canonical_nucleus(op.block(ca.I, J), r)
+    A, B = rank_r_factors(op.cols(J), op.rows(ca.I), Sr, sr, Tr)
+    num2, den2 = cur_residual(W, A, B)
+    return CurResult(ca.I, J, U, A, B, num2, den2, ca, Y)
+
+
 # ============================================================ canonical nucleus
 def canonical_nucleus(G: np.ndarray, r: int):
     """Alg 3.1 (algcnnncl): U = W_{k,l,r}⁺ from the SVD G = S Σ Tᵀ truncated to

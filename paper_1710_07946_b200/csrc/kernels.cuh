@@ -138,6 +138,9 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
 cudaError_t launch_error_sample(const OpView &op, const double *A, const double *B, int r, const int64_t *rows,
                                 int64_t q, const int64_t *cols, int64_t s, double *g, double *out3, cudaStream_t st,
                                 int *nlaunch, Prof *pf);
+// NEXT-3 greedy column expansion (expand.cu); scratch: (k n + k k + n) doubles
+cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
+                                  void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,
                               double *out3, cudaStream_t st);
 cudaError_t launch_sampled(const OpView &op, const double *A, const double *B, int r, const int64_t *si,

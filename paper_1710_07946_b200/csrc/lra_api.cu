@@ -827,6 +827,65 @@ lra_status lra_cur_certificate(lra_handle h, const lra_operand *W, const int64_t
   return LRA_OK;
 }
 
+lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t g0,
+                              int64_t l, double tie_slack, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "column expansion is not row-sharded");
+  if (!I || !J || k < 1 || k > 128 || g0 < k || l < g0 || l > W->n || !(tie_slack >= 0.0 && tie_slack < 1.0))
+    return fail(LRA_EINVAL, "need 1 <= k <= 128, k <= g0 <= l <= n");
+  if ((st = ws_reserve(h, ((size_t)k * W->n + (size_t)k * k + W->n) * 8 + 512)) != LRA_OK) return st;
+  int *ok = (int *)((char *)h->ws + (((size_t)k * W->n + (size_t)k * k + W->n) * 8 + 255) / 256 * 256);
+  int nl = 0;
+  CK(launch_expand_columns(make_view(W), I, (int)k, J, (int)g0, (int)l, tie_slack, h->ws, ok, (cudaStream_t)stream, &nl,
+                           &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, int64_t k,
+                               int64_t l, int64_t r, double *U, double *A, double *B, int32_t *status, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "use lra_cross_approx for row-sharded operands");
+  if (!I || !J || !A || !B || !status || k < 1 || l < 1 || k > 128 || l > 128 || r < 1 || r > (k < l ? k : l))
+    return fail(LRA_EINVAL, "need 0 < r <= min(k, l), k, l <= 128");
+  if ((st = ws_reserve(h, (size_t)(k + l) * r * 8 + 512)) != LRA_OK) return st;
+  double *TS = (double *)h->ws;
+  double *Sr = TS + (size_t)l * r;
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t), sm));
+  NucArgs na{};
+  na.op = make_view(W);
+  na.I = I;
+  na.J = J;
+  na.k = (int)k;
+  na.l = (int)l;
+  na.r = (int)r;
+  na.U = U;
+  na.TS = TS;
+  na.Sr = Sr;
+  na.status = status;
+  FacArgs fa{};
+  fa.op = na.op;
+  fa.I = I;
+  fa.J = J;
+  fa.k = (int)k;
+  fa.l = (int)l;
+  fa.r = (int)r;
+  fa.TS = TS;
+  fa.Sr = Sr;
+  fa.A = A;
+  fa.B = B;
+  fa.status = status;
+  int nl = 0;
+  CK(launch_nucleus(na, fa, 1, sm, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
 // inverse of the standard normal CDF (Acklam's rational approximation, |rel err| < 1.2e-9)
 static double norm_ppf(double p) {
   static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,

@@ -30,9 +30,14 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   extern __shared__ __align__(16) double nsm[];
   const int64_t b = blockIdx.x;
   if (a.status[b] != LRA_OK) return;
-  const int k = a.k, l = a.l, r = a.r;
+  const int r = a.r;
+  // A wide generator (k < l, NEXT-3 rectangular case) is handled through its transpose so
+  // that Jacobi always orthogonalises the shorter dimension: H = G^T = S' Sigma V^T gives
+  // G = V Sigma S'^T, i.e. S = V and T = S' (columns of the rotated H over sigma).
+  const bool tr = a.k < a.l;
+  const int k = tr ? a.l : a.k, l = tr ? a.k : a.l;   // H is k x l, k >= l
   const int L = (l + 1) & ~1;          // even number of columns (zero pad)
-  const int ldg = k;                   // G column stride
+  const int ldg = k;                   // H column stride
   double *G = nsm;                     // L columns of length k
   double *V = G + (size_t)L * ldg;     // L x L
   double *sig = V + (size_t)L * L;     // L
@@ -40,11 +45,12 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   __shared__ int s_rot;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
-  const int64_t *I = a.I + b * k, *J = a.J + b * l;
+  const int64_t *I = a.I + b * a.k, *J = a.J + b * a.l;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < L * k; e += NT) {
-    int j = e / k, i = e % k;
-    G[e] = j < l ? (a.Gd ? a.Gd[(size_t)b * k * l + e] : op.at(I[i], J[j])) : 0.0;
+    int j = e / k, i = e % k;          // H[i, j] = tr ? G[j, i] : G[i, j]
+    const int gi = tr ? j : i, gj = tr ? i : j;
+    G[e] = j < l ? (a.Gd ? a.Gd[(size_t)b * k * l + (size_t)gj * a.k + gi] : op.at(I[gi], J[gj])) : 0.0;
   }
   for (int e = tid; e < L * L; e += NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
   __syncthreads();
@@ -145,30 +151,32 @@ __global__ void __launch_bounds__(NUC_NT) k_nucleus(NucArgs a) {
   }
   __syncthreads();
   if (a.status[b] != LRA_OK) return;
-  double *TS = a.TS + b * (int64_t)l * r, *Sr = a.Sr + b * (int64_t)k * r;
-  for (int e = tid; e < l * r; e += NT) {      // TS[j, t] = T[j, ord t] / sigma
-    int t = e / l, j = e % l;
+  const int gk = a.k, gl = a.l;        // G's own shape
+  double *TS = a.TS + b * (int64_t)gl * r, *Sr = a.Sr + b * (int64_t)gk * r;
+  for (int e = tid; e < gl * r; e += NT) {     // TS[j, t] = T[j, ord t] / sigma
+    int t = e / gl, j = e % gl;
     int c = ord[t];
-    TS[(size_t)t * l + j] = V[(size_t)c * L + j] / sig[c];
+    TS[(size_t)t * gl + j] = tr ? G[(size_t)c * ldg + j] / (sig[c] * sig[c]) : V[(size_t)c * L + j] / sig[c];
   }
-  for (int e = tid; e < k * r; e += NT) {      // Sr[i, t] = G[i, ord t] / sigma
-    int t = e / k, i = e % k;
+  for (int e = tid; e < gk * r; e += NT) {     // Sr[i, t] = S[i, ord t]
+    int t = e / gk, i = e % gk;
     int c = ord[t];
-    Sr[(size_t)t * k + i] = G[(size_t)c * ldg + i] / sig[c];
+    Sr[(size_t)t * gk + i] = tr ? V[(size_t)c * L + i] : G[(size_t)c * ldg + i] / sig[c];
   }
   __syncthreads();
   if (a.U) {
-    double *U = a.U + b * (int64_t)l * k;
-    for (int e = tid; e < l * k; e += NT) {    // U (l x k, col-major) = TS * Sr^T
-      int col = e / l, row = e % l;
+    double *U = a.U + b * (int64_t)gl * gk;
+    for (int e = tid; e < gl * gk; e += NT) {  // U (l x k, col-major) = TS * Sr^T
+      int col = e / gl, row = e % gl;
       double s = 0.0;
-      for (int t = 0; t < r; ++t) s = fma(TS[(size_t)t * l + row], Sr[(size_t)t * k + col], s);
-      U[(size_t)col * l + row] = s;
+      for (int t = 0; t < r; ++t) s = fma(TS[(size_t)t * gl + row], Sr[(size_t)t * gk + col], s);
+      U[(size_t)col * gl + row] = s;
     }
   }
 }
 
 size_t nucleus_smem(int k, int l) {
+  if (k < l) { int t = k; k = l; l = t; }     // transposed wide case
   int L = (l + 1) & ~1;
   return ((size_t)L * k + (size_t)L * L + L) * 8 + (size_t)L * 4 + 16;
 }
@@ -260,7 +268,7 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   cudaError_t e = cudaFuncSetAttribute(k_nucleus, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   pf->begin("k_nucleus", st);
-  const int L = (na.l + 1) & ~1;
+  const int L = ((na.k < na.l ? na.k : na.l) + 1) & ~1;
   int nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
   if (nt > 1024) nt = 1024;
   k_nucleus<<<(unsigned)nb, nt, smem, st>>>(na);

@@ -78,6 +78,10 @@ def _load():
     lib.lra_preprocess_full.restype = C.c_int
     lib.lra_error_sample.argtypes = [vp, P(lra_operand), vp, vp, i64, vp, i64, vp, i64, vp, vp]
     lib.lra_error_sample.restype = C.c_int
+    lib.lra_expand_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i64, dbl, vp]
+    lib.lra_expand_columns.restype = C.c_int
+    lib.lra_nucleus_factors.argtypes = [vp, P(lra_operand), vp, vp, i64, i64, i64, vp, vp, vp, vp, vp]
+    lib.lra_nucleus_factors.restype = C.c_int
     lib.lra_cur_certificate.argtypes = [vp, P(lra_operand), vp, vp, vp, i64, i64, i64, dbl, P(C.c_double), vp]
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
@@ -113,7 +117,7 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
-            "lra_cur_certificate"]
+            "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors"]
 
 
 def debug_counters(reset=True):
@@ -294,6 +298,18 @@ def lra_cross_approx(h, W, Y, I0, r, k, l, sweeps, I, J, U, A, B, stats=None, y_
 def lra_cur_residual(h, W, A, B, r, num2, den2, nsamples=0, si=None, sj=None, prec=LRA_RECON_PRECISE, stream=None):
     _check(lib().lra_cur_residual(h.h, C.byref(W.struct()), _ptr(A), _ptr(B), r, prec, nsamples, _ptr(si), _ptr(sj),
                                   _ptr(num2), _ptr(den2), _stream(stream)))
+
+
+def lra_expand_columns(h, W, I, J, g0, tie_slack=1e-12, stream=None):
+    """J (l,) int64 device tensor: first g0 entries given, the rest filled greedily (Alg D.4)."""
+    _check(lib().lra_expand_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), _ptr(J), g0, J.numel(), tie_slack,
+                                    _stream(stream)))
+
+
+def lra_nucleus_factors(h, W, I, J, r, U, A, B, status, stream=None):
+    """U (k, l) storage of the l x k nucleus, A (r, m), B (n, r); status (1,) int32."""
+    _check(lib().lra_nucleus_factors(h.h, C.byref(W.struct()), _ptr(I), _ptr(J), I.numel(), J.numel(), r, _ptr(U),
+                                     _ptr(A), _ptr(B), _ptr(status), _stream(stream)))
 
 
 def lra_cur_certificate(h, W, I, J, U, k, l, r, delta, stream=None):

@@ -95,3 +95,23 @@ def cur_progressive(h, W, r, k, sweeps, tol, seed, rows, cols, dmax=6, stream=No
         if est <= tol or d >= dmax or W.n % (1 << (d + 1)):
             return d, bufs, est
         d += 1
+
+
+def cur_rectangular(h, W, M, r, k, l, sweeps, stream=None):
+    """k x l generators, l > k (NEXT-3): the square C-A (k = k) of Alg 10.2, Alg D.4 greedy
+    expansion of J to l columns, then the canonical nucleus / factors of the k x l generator
+    and the a-posteriori check.  Returns (square bufs, J (l,), U (k, l), A, B, num2, den2)."""
+    bufs = cur(h, W, M, r, k, sweeps, stream=stream)
+    dev = bufs.I.device
+    J = torch.empty(l, dtype=torch.int64, device=dev)
+    J[:k] = bufs.J
+    L.lra_expand_columns(h, W, bufs.I, J, k, stream=stream)
+    U = torch.empty((k, l), dtype=torch.float64, device=dev)
+    A = torch.empty((r, W.m), dtype=torch.float64, device=dev)
+    B = torch.empty((W.n, r), dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    L.lra_nucleus_factors(h, W, bufs.I, J, r, U, A, B, status, stream=stream)
+    num2 = torch.empty(1, dtype=torch.float64, device=dev)
+    den2 = torch.empty(1, dtype=torch.float64, device=dev)
+    L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
+    return bufs, J, U, A, B, num2, den2

@@ -586,3 +586,28 @@ def test_config5_full_size_invariants():
     out = json.loads(p.stdout.strip().splitlines()[-1])
     assert out["status"] == 0 and out["sketch_rows_exact"]
     assert out["cert_rows"] <= 1 + 1e-12 and out["cert_cols"] <= 1 + 1e-12
+
+
+# ------------------------------------------------------------ NEXT-3: rectangular generators
+@pytest.mark.parametrize("case", ["small", "config2"])
+def test_rectangular_generators_vs_oracle(P, h, case):
+    """k x l generators (l > k) by Alg D.4 greedy expansion after the square C-A: the expanded
+    columns, pivots, nucleus and rho equal the oracle's (rho to 1e-4 on fp32 data).  k is at
+    most the numerical rank (reading C28: beyond it the expansion scores are rounding noise
+    amplified by cond(G G^T) and no two fp64 implementations agree on the pick)."""
+    from paper_1710_07946_b200 import pipeline
+    if case == "small":
+        W = synth.factor_gaussian(6, 600, 500, 8, 1e-9)
+        M, r, k, l = synth.multiplier_abridged(6, 500, 2, 8, "arht"), 7, 8, 13
+    else:
+        W = synth.config2(0)
+        M, r, k, l = synth.multiplier_abridged(0, 4096, 4, 32, "arht"), 32, 32, 48
+    ora = O.cur_rectangular(W, M, r, k, l, 3)
+    bufs, J, U, A, B, num2, den2 = pipeline.cur_rectangular(h, _dense(P, W), P.lra.Multiplier(M), r, k, l, 3)
+    torch.cuda.synchronize()
+    assert list(bufs.I.cpu().numpy()) == list(ora.I)
+    assert list(J.cpu().numpy()) == list(ora.J)
+    Ug = U.cpu().numpy().T
+    assert np.allclose(Ug, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
+    rho = float(np.sqrt(num2.item() / den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)

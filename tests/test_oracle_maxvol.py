@@ -131,3 +131,37 @@ def test_ca_log_volume_monotone_and_fixed_point(seed):
     ca2 = lra.cross_approx(op, 6, 6, 2, I0=ca.I, J0=ca.J)
     assert list(ca2.I) == list(ca.I) and list(ca2.J) == list(ca.J)
     assert all(sw == 0 for _, sw in ca2.steps)
+
+
+# ------------------------------------------------------------ NEXT-3: greedy expansion (Alg D.4)
+def test_expand_columns_volume_identity_and_brute_force():
+    """Each appended column multiplies v2(C)^2 = det(C C^T) by exactly 1 + score (eq. eqbun),
+    and is the argmax of det over all candidates (brute force)."""
+    g = np.random.default_rng(12)
+    R = g.standard_normal((4, 30))
+    J0 = [3, 7, 11, 20]
+    J, scores = lra.expand_columns(R, J0, 8)
+    assert list(J[:4]) == J0 and len(set(J.tolist())) == 8
+    for step in range(4):
+        cur = list(J[:4 + step])
+        C = R[:, cur]
+        d0 = np.linalg.det(C @ C.T)
+        dets = np.full(30, -np.inf)
+        for j in range(30):
+            if j not in cur:
+                Cj = R[:, cur + [j]]
+                dets[j] = np.linalg.det(Cj @ Cj.T)
+        assert int(np.argmax(dets)) == J[4 + step]
+        assert dets[J[4 + step]] / d0 == pytest.approx(1 + scores[step], rel=1e-10)
+
+
+def test_rectangular_generator_exact_recovery_and_improvement():
+    """k x l generators (l > k) still reproduce a rank-r W exactly (thm thcandec) and the
+    expansion never lowers v2 of the generator."""
+    W = synth.factor_gaussian(6, 200, 180, 5, 0.0)
+    mult = synth.multiplier_abridged(6, 180, 2, 5, "arht")
+    res = lra.cur_rectangular(W, mult, 5, 5, 9, 2)
+    assert len(res.J) == 9 and res.rho < 1e-12
+    G5 = W[np.ix_(res.I, res.J[:5])]
+    G9 = W[np.ix_(res.I, res.J)]
+    assert np.linalg.det(G9 @ G9.T) >= np.linalg.det(G5 @ G5.T) * (1 - 1e-12)
