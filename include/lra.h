@@ -122,6 +122,18 @@ lra_status lra_handle_create(lra_handle *h /* host */, int device, const void *n
 lra_status lra_nccl_unique_id(void *out /* host, 128 bytes */);
 void lra_handle_destroy(lra_handle h);
 
+/* Scratch of one workload shape (SURVEY 8(b) "lra_workspace_query"; the handle owns every
+   scratch buffer and grows it on first use).  nb == 0: the single-problem calls
+   lra_preprocess / lra_cross_approx (sweeps) / lra_cur_residual (either lra_recon) on W with
+   rank r and k = l; nb >= 1: lra_batch over nb blocks shaped like W.  *bytes (host) = the
+   device bytes those calls need.  lra_workspace_reserve allocates them now, so the calls of
+   that shape allocate nothing (and can be captured in a CUDA graph).  Errors: EINVAL for a
+   bad operand/shape (the checks of lra_cross_approx), ENOMEM. */
+lra_status lra_workspace_query(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps,
+                               int64_t nb, size_t *bytes /* host */);
+lra_status lra_workspace_reserve(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps,
+                                 int64_t nb);
+
 /* Stage 1 of Alg 10.2: Y = W * M, an m x lbar fp64 column-major matrix
    (ARFT: complex128, interleaved re/im), leading dimension ldy >= m.  Sums run in a fixed
    order (ascending t for ARHT/ARFT, draw order for SPARSE_PM1, ascending k for GAUSSIAN)

@@ -114,6 +114,21 @@ static lra_status ws_reserve(lra_handle h, size_t bytes) {
   return LRA_OK;
 }
 
+// Exact-size reservation of one of the handle's secondary device buffers (grid-tier exchange,
+// global-memory C-A tier, sharded blocks).
+static lra_status buf_reserve(void **buf, size_t *have, size_t bytes, const char *what) {
+  if (bytes <= *have) return LRA_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  if (cudaMalloc(buf, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LRA_ENOMEM, "cannot allocate %zu bytes for %s", bytes, what);
+  }
+  *have = bytes;
+  return LRA_OK;
+}
+
 struct Carve {
   char *base;
   size_t off;
@@ -424,36 +439,17 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   ca.status = status;
   ca.yinfo = y_complex ? yinfo : nullptr;
   ca.grid = 0;
-  {
-    const size_t gb = ca_grid_scratch_bytes(160);
-    if (h->gs_bytes < gb) {
-      if (h->gs) cudaFree(h->gs);
-      h->gs = nullptr;
-      h->gs_bytes = 0;
-      if (cudaMalloc(&h->gs, gb) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LRA_ENOMEM, "cannot allocate the grid-tier exchange buffers");
-      }
-      h->gs_bytes = gb;
-    }
-    ca.gscratch = h->gs;
-  }
+  lra_status rs;
+  if ((rs = buf_reserve(&h->gs, &h->gs_bytes, ca_grid_scratch_bytes(160), "the grid-tier exchange")) != LRA_OK)
+    return rs;
+  ca.gscratch = h->gs;
   int cs = 0;
   const int64_t maxN = W->m > W->n ? W->m : W->n;
   cudaError_t e;
   if (ca_needs_global(maxN, (int)k)) {
     if (y_complex) return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
-    const size_t gb = ca_global_scratch_bytes(maxN, (int)k);
-    if (h->gm_bytes < gb) {
-      if (h->gm) cudaFree(h->gm);
-      h->gm = nullptr;
-      h->gm_bytes = 0;
-      if (cudaMalloc(&h->gm, gb) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the global-memory C-A tier", gb);
-      }
-      h->gm_bytes = gb;
-    }
+    if ((rs = buf_reserve(&h->gm, &h->gm_bytes, ca_global_scratch_bytes(maxN, (int)k), "the global-memory C-A tier")) != LRA_OK)
+      return rs;
     e = launch_ca_global(ca, nb, maxN, h->gm, st, &h->prof);
     if (e == cudaSuccess) h->launches += nb;
   } else {
@@ -530,23 +526,29 @@ static lra_status maxvol_block(lra_handle h, const double *blk, int64_t N, int q
     int cs = 0;
     e = launch_ca_cluster(ca, 1, N, st, &cs, &h->prof);
   } else {
-    const size_t gb = ca_global_scratch_bytes(N, q);
-    if (h->gm_bytes < gb) {
-      if (h->gm) cudaFree(h->gm);
-      h->gm = nullptr;
-      h->gm_bytes = 0;
-      if (cudaMalloc(&h->gm, gb) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the global-memory C-A tier", gb);
-      }
-      h->gm_bytes = gb;
-    }
+    lra_status rs;
+    if ((rs = buf_reserve(&h->gm, &h->gm_bytes, ca_global_scratch_bytes(N, q), "the global-memory C-A tier")) != LRA_OK)
+      return rs;
     e = launch_ca_global(ca, 1, N, h->gm, st, &h->prof);
   }
   if (e == cudaErrorInvalidConfiguration) return fail(LRA_EUNSUPPORTED, "block %lld x %d exceeds the C-A tiers", (long long)N, q);
   CK(e);
   h->launches += 1;
   return LRA_OK;
+}
+
+static size_t sharded_scratch(int64_t M, int64_t n, int64_t r, int64_t q, int32_t sweeps) {
+  const int64_t Nmax = M > n ? M : n;
+  Carve probe{nullptr, 0};
+  probe.take<double>((size_t)Nmax * q);         // assembled block
+  probe.take<double>((size_t)n * q);            // R^T for the final factor B
+  probe.take<double>((size_t)q * q);            // G
+  probe.take<double>((size_t)q * r);            // TS
+  probe.take<double>((size_t)q * r);            // Sr
+  probe.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
+  probe.take<int32_t>(4);
+  probe.take<int64_t>((size_t)q);               // dummy J output of standalone maxvol calls
+  return probe.off + 256;
 }
 
 static lra_status allreduce_sum(lra_handle h, double *buf, size_t count, cudaStream_t st) {
@@ -562,26 +564,9 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
   if (!h->comm && h->nranks > 1) return fail(LRA_ENCCL, "row-sharded operand needs an NCCL communicator");
   const int64_t M = W->m_global, n = W->n, q = k;
   const int64_t Nmax = M > n ? M : n;
-  Carve probe{nullptr, 0};
-  probe.take<double>((size_t)Nmax * q);         // assembled block
-  probe.take<double>((size_t)n * q);            // R^T for the final factor B
-  probe.take<double>((size_t)q * q);            // G
-  probe.take<double>((size_t)q * r);            // TS
-  probe.take<double>((size_t)q * r);            // Sr
-  probe.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
-  probe.take<int32_t>(4);
-  probe.take<int64_t>((size_t)q);               // dummy J output of standalone maxvol calls
-  const size_t need = probe.off + 256;
-  if (h->sh_bytes < need) {
-    if (h->sh) cudaFree(h->sh);
-    h->sh = nullptr;
-    h->sh_bytes = 0;
-    if (cudaMalloc(&h->sh, need) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(LRA_ENOMEM, "cannot allocate %zu bytes for the sharded blocks", need);
-    }
-    h->sh_bytes = need;
-  }
+  lra_status rs;
+  if ((rs = buf_reserve(&h->sh, &h->sh_bytes, sharded_scratch(M, n, r, k, sweeps), "the sharded blocks")) != LRA_OK)
+    return rs;
   Carve cv{(char *)h->sh, 0};
   double *blk = cv.take<double>((size_t)Nmax * q);
   double *Rt = cv.take<double>((size_t)n * q);
@@ -692,6 +677,15 @@ done:
   return LRA_OK;
 }
 
+static size_t chain_scratch(int64_t r, int64_t k) {
+  Carve probe{nullptr, 0};
+  probe.take<int32_t>(1);
+  probe.take<double>((size_t)k * r);
+  probe.take<double>((size_t)k * r);
+  probe.take<int32_t>(4);
+  return probe.off + 256;
+}
+
 lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy, int y_complex,
                             const int64_t *I0, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
                             double tie_slack, int32_t swap_cap, int64_t *I, int64_t *J, double *U, double *A,
@@ -710,18 +704,8 @@ lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, i
     return sharded_cross_approx(h, W, Y, ldy, I0, r, k, sweeps, swap_tol, tie_slack, swap_cap, I, J, U, A, B,
                                 stats, (cudaStream_t)stream);
   }
-  Carve cv{nullptr, 0};
-  size_t need = 0;
-  {
-    Carve probe{nullptr, 0};
-    probe.take<int32_t>(1);
-    probe.take<double>((size_t)k * r);
-    probe.take<double>((size_t)k * r);
-    probe.take<int32_t>(4);
-    need = probe.off + 256;
-  }
-  if ((s = ws_reserve(h, need)) != LRA_OK) return s;
-  cv.base = (char *)h->ws;
+  if ((s = ws_reserve(h, chain_scratch(r, k))) != LRA_OK) return s;
+  Carve cv{(char *)h->ws, 0};
   int32_t *status = cv.take<int32_t>(1);
   double *TS = cv.take<double>((size_t)k * r);
   double *Sr = cv.take<double>((size_t)k * r);
@@ -922,6 +906,20 @@ lra_status lra_variance_bound(double var_K, int64_t K, double alpha, double *bou
   return LRA_OK;
 }
 
+static size_t batch_scratch(int64_t m, int64_t n, int64_t r, int64_t k, int64_t nb, size_t esz, int S) {
+  Carve probe{nullptr, 0};
+  probe.take<int32_t>(nb);
+  probe.take<char>((size_t)nb * m * k * esz);
+  probe.take<double>((size_t)nb * k * r);
+  probe.take<double>((size_t)nb * k * r);
+  probe.take<double>((size_t)nb * m * r);
+  probe.take<double>((size_t)nb * r * n);
+  probe.take<double2>((size_t)nb * resid_partials(m, n));
+  probe.take<int32_t>((size_t)nb * 4);
+  probe.take<char>(S ? residual_tc_scratch(m, n, (int)r, S, nb) : 0);
+  return probe.off + 256;
+}
+
 lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_stride, const lra_multiplier *M0,
                      int64_t m_stride, int64_t r, int64_t k, int64_t l, int32_t sweeps, double swap_tol,
                      double tie_slack, int32_t swap_cap, int32_t prec, int64_t *I, int64_t *J, double *U,
@@ -945,17 +943,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   const size_t esz = cplx ? 16 : 8;
   const int64_t tiles = resid_partials(m, n);
   const int S = resid_slices(W0->dtype, prec);
-  Carve probe{nullptr, 0};
-  probe.take<int32_t>(nb);
-  probe.take<char>((size_t)nb * m * k * esz);
-  probe.take<double>((size_t)nb * k * r);
-  probe.take<double>((size_t)nb * k * r);
-  probe.take<double>((size_t)nb * m * r);
-  probe.take<double>((size_t)nb * r * n);
-  probe.take<double2>((size_t)nb * tiles);
-  probe.take<int32_t>((size_t)nb * 4);
-  probe.take<char>(S ? residual_tc_scratch(m, n, (int)r, S, nb) : 0);
-  if ((s = ws_reserve(h, probe.off + 256)) != LRA_OK) return s;
+  if ((s = ws_reserve(h, batch_scratch(m, n, r, k, nb, esz, S))) != LRA_OK) return s;
   Carve cv{(char *)h->ws, 0};
   int32_t *status = cv.take<int32_t>(nb);
   void *Y = cv.take<char>((size_t)nb * m * k * esz);
@@ -1038,6 +1026,66 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
     CK(cudaEventRecord(h->join[i], h->side[i]));
     CK(cudaStreamWaitEvent(st, h->join[i], 0));
   }
+  return LRA_OK;
+}
+
+// Scratch for the calls of one workload shape (reading of SURVEY 8(b) "lra_workspace_query"):
+// nb == 0 sizes lra_preprocess / lra_cross_approx / lra_cur_residual (either lra_recon) on W;
+// nb >= 1 sizes lra_batch over nb blocks shaped like W.  All four handle-owned buffers count.
+static lra_status workspace_sizes(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps,
+                                  int64_t nb, size_t sz[4]) {
+  (void)h;
+  lra_status s;
+  if ((s = check_operand(W)) != LRA_OK) return s;
+  if ((s = check_ca_shape(W, r, k, k, sweeps)) != LRA_OK) return s;
+  if (nb < 0) return fail(LRA_EINVAL, "nb >= 0");
+  const int64_t m = W->m, n = W->n, mg = W->m_global > 0 ? W->m_global : m;
+  const int64_t maxN = mg > n ? mg : n;
+  size_t ws = 0, gm = 0, sh = 0;
+  const int Smax = W->dtype == LRA_F32 ? 6 : 3;
+  if (nb == 0) {
+    ws = chain_scratch(r, k);
+    if (W->kind == LRA_OP_DENSE) {
+      const size_t rs = resid_scratch(m, n, r, Smax, 1), r0 = resid_scratch(m, n, r, 0, 1);
+      ws = ws > rs ? ws : rs;
+      ws = ws > r0 ? ws : r0;
+    }
+    const size_t smp = (size_t)2 * 296 * sizeof(double2) + 256;
+    ws = ws > smp ? ws : smp;
+    if (W->m_global > 0) sh = sharded_scratch(mg, n, r, k, sweeps);
+    if (ca_needs_global(maxN, (int)k) || W->m_global > 0) gm = ca_global_scratch_bytes(maxN, (int)k);
+  } else {
+    if (W->kind != LRA_OP_DENSE || W->m_global > 0) return fail(LRA_EINVAL, "lra_batch takes unsharded dense blocks");
+    const size_t a = batch_scratch(m, n, r, k, nb, 16, Smax), b = batch_scratch(m, n, r, k, nb, 16, 0);
+    ws = a > b ? a : b;
+    if (ca_needs_global(maxN, (int)k)) gm = ca_global_scratch_bytes(maxN, (int)k);
+  }
+  sz[0] = ws + ws / 4;   // ws_reserve over-allocates by a quarter
+  sz[1] = ca_grid_scratch_bytes(160);
+  sz[2] = gm;
+  sz[3] = sh;
+  return LRA_OK;
+}
+
+lra_status lra_workspace_query(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps, int64_t nb,
+                               size_t *bytes) {
+  if (!h || !bytes) return fail(LRA_EINVAL, "null handle or bytes");
+  size_t sz[4];
+  lra_status s;
+  if ((s = workspace_sizes(h, W, r, k, sweeps, nb, sz)) != LRA_OK) return s;
+  *bytes = sz[0] + sz[1] + sz[2] + sz[3];
+  return LRA_OK;
+}
+
+lra_status lra_workspace_reserve(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps, int64_t nb) {
+  lra_status s;
+  if ((s = check_device(h)) != LRA_OK) return s;
+  size_t sz[4];
+  if ((s = workspace_sizes(h, W, r, k, sweeps, nb, sz)) != LRA_OK) return s;
+  if ((s = ws_reserve(h, sz[0] * 4 / 5)) != LRA_OK) return s;
+  if ((s = buf_reserve(&h->gs, &h->gs_bytes, sz[1], "the grid-tier exchange")) != LRA_OK) return s;
+  if (sz[2] && (s = buf_reserve(&h->gm, &h->gm_bytes, sz[2], "the global-memory C-A tier")) != LRA_OK) return s;
+  if (sz[3] && (s = buf_reserve(&h->sh, &h->sh_bytes, sz[3], "the sharded blocks")) != LRA_OK) return s;
   return LRA_OK;
 }
 

@@ -86,6 +86,10 @@ def _load():
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
+    lib.lra_workspace_query.argtypes = [vp, P(lra_operand), i64, i64, i32, i64, P(C.c_size_t)]
+    lib.lra_workspace_query.restype = C.c_int
+    lib.lra_workspace_reserve.argtypes = [vp, P(lra_operand), i64, i64, i32, i64]
+    lib.lra_workspace_reserve.restype = C.c_int
     lib.lra_nccl_unique_id.argtypes = [vp]
     lib.lra_nccl_unique_id.restype = C.c_int
     lib.lra_launch_count.argtypes = [vp]
@@ -117,7 +121,8 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
-            "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors"]
+            "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
+            "lra_workspace_reserve"]
 
 
 def debug_counters(reset=True):
@@ -272,6 +277,18 @@ class Handle:
 
 def lra_handle_create(device=0):
     return Handle(device)
+
+
+def lra_workspace_query(h, W, r, k, sweeps, nb=0):
+    """Device scratch bytes of the calls of this shape (nb = 0: single problem; nb >= 1: lra_batch)."""
+    out = C.c_size_t(0)
+    _check(lib().lra_workspace_query(h.h, C.byref(W.struct()), int(r), int(k), int(sweeps), int(nb), C.byref(out)))
+    return int(out.value)
+
+
+def lra_workspace_reserve(h, W, r, k, sweeps, nb=0):
+    """Allocate that scratch now (the calls of this shape then allocate nothing)."""
+    _check(lib().lra_workspace_reserve(h.h, C.byref(W.struct()), int(r), int(k), int(sweeps), int(nb)))
 
 
 def lra_preprocess(h, W, M, Y, stream=None):

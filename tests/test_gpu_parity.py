@@ -611,3 +611,59 @@ def test_rectangular_generators_vs_oracle(P, h, case):
     assert np.allclose(Ug, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
     rho = float(np.sqrt(num2.item() / den2.item()))
     assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
+
+
+# ------------------------------------------------------------ workspace query / graph capture
+@pytest.mark.parametrize("nb", [0, 5])
+def test_workspace_query_reserve_and_graph_capture(P, nb):
+    """lra_workspace_query/lra_workspace_reserve: after the reserve, the calls of
+    that shape allocate nothing, so the whole chain captures into a CUDA graph; replaying the
+    graph reproduces the eager outputs bit for bit (and the eager outputs equal the oracle)."""
+    from paper_1710_07946_b200 import pipeline
+    L = P.lra
+    h2 = P.Handle(0)
+    W = synth.config1(0)
+    M = synth.multiplier_abridged(0, 256, 3, 8, "arht")
+    Wd, Md = _dense(P, W), L.Multiplier(M)
+    if nb == 0:
+        need = L.lra_workspace_query(h2, Wd, 8, 8, 2)
+        assert need > 0
+        L.lra_workspace_reserve(h2, Wd, 8, 8, 2)
+        bufs = pipeline.CurBuffers(256, 256, 8, 8)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            pipeline.cur(h2, Wd, Md, 8, 8, 2, bufs=bufs)
+        torch.cuda.synchronize()
+        eager = (bufs.I.clone(), bufs.J.clone(), bufs.U.clone(), bufs.num2.clone())
+        ora = O.cur_pipeline(W, M, 8, 8, 8, 2)
+        assert list(eager[0].cpu().numpy()) == list(ora.I)
+        for t in (bufs.I, bufs.J, bufs.U, bufs.num2):
+            t.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            pipeline.cur(h2, Wd, Md, 8, 8, 2, bufs=bufs)
+        g.replay()
+        torch.cuda.synchronize()
+        for a, b in zip(eager, (bufs.I, bufs.J, bufs.U, bufs.num2)):
+            assert torch.equal(a, b)
+    else:
+        Wb = np.stack([synth.config1(s) for s in range(nb)])
+        Wt = torch.from_numpy(np.ascontiguousarray(np.transpose(Wb, (0, 2, 1)))).cuda()
+        Wbatch = L.Dense(Wt)
+        assert L.lra_workspace_query(h2, Wbatch, 8, 8, 2, nb) > L.lra_workspace_query(h2, Wbatch, 8, 8, 2, 1)
+        L.lra_workspace_reserve(h2, Wbatch, 8, 8, 2, nb)
+        bb = pipeline.BatchBuffers(nb, 8, 8)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            pipeline.cur_batch(h2, Wbatch, Md, 8, 8, 2, nb, bufs=bb)
+        torch.cuda.synchronize()
+        eager = (bb.I.clone(), bb.num2.clone())
+        bb.I.zero_()
+        bb.num2.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            pipeline.cur_batch(h2, Wbatch, Md, 8, 8, 2, nb, bufs=bb)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(eager[0], bb.I) and torch.equal(eager[1], bb.num2)
+    h2.close()
