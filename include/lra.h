@@ -194,7 +194,8 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
 lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t g0,
                               int64_t l, double tie_slack, void *stream);
 /* Canonical nucleus U = W_{k,l,r}^+ (Alg 3.1) of the generator W[I,J] (any k x l,
-   k, l <= 128) and the factors A = W[:,J] T_r Sigma_r^{-1} (m x r), B = S_r^T W[I,:] (r x n),
+   k, l <= 128 whose Jacobi working set min(k,l)+1 columns of max(k,l) plus the rotation matrix
+   fits in shared memory: square k = l <= 112; EUNSUPPORTED otherwise) and the factors A = W[:,J] T_r Sigma_r^{-1} (m x r), B = S_r^T W[I,:] (r x n),
    as lra_cross_approx computes them for k = l.  status (device int32): LRA_OK or ESINGULAR. */
 lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, int64_t k,
                                int64_t l, int64_t r, double *U, double *A, double *B, int32_t *status, void *stream);

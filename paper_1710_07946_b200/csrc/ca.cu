@@ -1169,6 +1169,9 @@ cudaError_t read_ca_counters(unsigned long long *out, bool reset) {
   if (e == cudaSuccess) e = read_cc_counters(c2, reset);
   if (e == cudaSuccess)
     for (int i = 0; i < 16; ++i) out[i] += c2[i];
+  unsigned long long nc[2];
+  if (e == cudaSuccess) e = read_nuc_counters(nc, reset);
+  if (e == cudaSuccess) { out[14] = nc[0]; out[15] = nc[1]; }
   return e;
 }
 

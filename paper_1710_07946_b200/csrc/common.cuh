@@ -8,7 +8,7 @@
 
 #define LRA_NT 512          // threads of the maxvol / C-A CTAs
 #define LRA_QMAX 64         // largest k = l handled by the on-chip (cluster / grid) tiers
-#define LRA_QMAX_ALL 128    // largest k = l handled at all (global-memory tier)
+#define LRA_QMAX_ALL 112    // largest k = l handled at all (global-memory tier; the nucleus's H and V fit in shared memory)
 
 // ----------------------------------------------------------------------------- complex
 struct cplx {

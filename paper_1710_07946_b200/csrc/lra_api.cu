@@ -836,6 +836,7 @@ lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t
   if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "use lra_cross_approx for row-sharded operands");
   if (!I || !J || !A || !B || !status || k < 1 || l < 1 || k > 128 || l > 128 || r < 1 || r > (k < l ? k : l))
     return fail(LRA_EINVAL, "need 0 < r <= min(k, l), k, l <= 128");
+  if (!nucleus_fits((int)k, (int)l)) return fail(LRA_EUNSUPPORTED, "a %lld x %lld generator exceeds the nucleus's shared memory", (long long)k, (long long)l);
   if ((st = ws_reserve(h, (size_t)(k + l) * r * 8 + 512)) != LRA_OK) return st;
   double *TS = (double *)h->ws;
   double *Sr = TS + (size_t)l * r;

@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liblra.so")
+_SO = os.environ.get("LRA_SO") or os.path.join(_HERE, "liblra.so")   # LRA_SO: diagnostics (A/B builds)
 
 LRA_OK, LRA_EINVAL, LRA_ESINGULAR, LRA_ENOMEM, LRA_ECUDA, LRA_ENCCL, LRA_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 LRA_F32, LRA_F64 = 0, 1
@@ -86,10 +86,11 @@ def _load():
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
-    lib.lra_workspace_query.argtypes = [vp, P(lra_operand), i64, i64, i32, i64, P(C.c_size_t)]
-    lib.lra_workspace_query.restype = C.c_int
-    lib.lra_workspace_reserve.argtypes = [vp, P(lra_operand), i64, i64, i32, i64]
-    lib.lra_workspace_reserve.restype = C.c_int
+    if hasattr(lib, "lra_workspace_query"):   # absent from older builds loaded through LRA_SO
+        lib.lra_workspace_query.argtypes = [vp, P(lra_operand), i64, i64, i32, i64, P(C.c_size_t)]
+        lib.lra_workspace_query.restype = C.c_int
+        lib.lra_workspace_reserve.argtypes = [vp, P(lra_operand), i64, i64, i32, i64]
+        lib.lra_workspace_reserve.restype = C.c_int
     lib.lra_nccl_unique_id.argtypes = [vp]
     lib.lra_nccl_unique_id.restype = C.c_int
     lib.lra_launch_count.argtypes = [vp]
@@ -129,7 +130,7 @@ def debug_counters(reset=True):
     out = (C.c_uint64 * 16)()
     _check(lib().lra_debug_counters(out, int(reset)))
     names = ["load", "cold_lu", "warm_gather", "gauss_jordan", "product", "swap_loop", "kernel", "pivot_steps",
-             "exact_rounds", "pk_reduce", "pk_cluster_bar", "pk_decide", "take_row", "sw_update", "-", "-"]
+             "exact_rounds", "pk_reduce", "pk_cluster_bar", "pk_decide", "take_row", "sw_update", "nuc_sweeps", "nuc_rotations"]
     return dict(zip(names, [int(x) for x in out]))
 
 

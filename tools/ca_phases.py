@@ -23,5 +23,5 @@ torch.cuda.synchronize()
 prof = h.profile_read()
 cnt = lra.debug_counters(reset=True)
 st = lra.stats_to_numpy(bufs.stats)[0]
-out = {k: (v / 1965.0 if k != "pivot_steps" else v) for k, v in cnt.items()}
+out = {k: (v / 1965.0 if k not in ("pivot_steps", "nuc_sweeps", "nuc_rotations") else v) for k, v in cnt.items()}
 print(json.dumps({"phases_us": out, "kernels_ms": prof, "swaps": int(st["swaps"]), "lu": int(st["lu_steps"])}, indent=1))
