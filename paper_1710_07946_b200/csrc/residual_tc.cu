@@ -22,6 +22,8 @@
 // the four warps drain TMEM (tcgen05.ld 32x32b, warp w owns rows 32w..32w+31).
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace lra {
 // phase counters (clock64 cycles summed over CTAs): 0 MMA wait B, 1 MMA wait TMEM, 2 MMA issue,
 // 3 producer wait B stage, 4 producer wait A, 5 MMA wait A, 6 epilogue wait TMEM (warp 0),
@@ -165,6 +167,88 @@ __global__ void __launch_bounds__(2 * BN) k_split_b(const double *B, int64_t n, 
     for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint4 *>(base + (size_t)(kb * S + s) * B_TILE + (jj >> 3) * 256 + h * 128 + (jj & 7) * 16) =
           make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
+// One launch for both factors (grid.x = RB + ceil(CB / 4), grid.y = nb, 128 threads), every
+// input value loaded exactly once into registers (all r loads in flight):
+//  - A CTAs: thread = one row of a 128-row block; the row exponent from its r values;
+//  - B CTAs: 4 warps = 4 tiles of 32 columns, thread = one column; the tile exponent is the
+//    warp max of the column maxima.
+// The digits are the same as k_split_a / k_split_b (same exponents, same digit recurrence),
+// written to the same canonical layout.
+template <int KBT>
+__global__ void __launch_bounds__(128) k_split_ab(const double *A, const double *B, int64_t m, int64_t n, int r,
+                                                  int64_t a_stride, int64_t b_stride, int S, int64_t RB, int64_t CB,
+                                                  signed char *Aq, signed char *Bq, int *sa, int *sbq,
+                                                  const int32_t *status) {
+  constexpr int RT = KBT * BK;                 // values per thread (zero beyond r)
+  const int64_t b = blockIdx.y;
+  const bool live = !(status && status[b] != LRA_OK);
+  double v[RT];
+  double mx = 0.0;
+  signed char *base;
+  int boff;
+  int tile_bytes;
+  if ((int64_t)blockIdx.x < RB) {
+    const int64_t rb = blockIdx.x;
+    const int i = threadIdx.x;
+    const int64_t gi = rb * BM + i;
+    const bool ok = live && gi < m;
+    const double *Ab = A + b * a_stride + gi;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) v[t] = (ok && t < r) ? __ldg(Ab + (int64_t)t * m) : 0.0;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) mx = fmax(mx, fabs(v[t]));
+    const int e = scale_exp(mx);
+    if (gi < m) sa[b * m + gi] = ok ? e : -4000;     // -4000: row contributes nothing
+    const double p2 = ldexp(1.0, -e);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) v[t] *= p2;
+    base = Aq + (size_t)(b * RB + rb) * KBT * S * A_TILE;
+    boff = (i >> 3) * 256 + (i & 7) * 16;
+    tile_bytes = A_TILE;
+  } else {
+    const int64_t cb = ((int64_t)blockIdx.x - RB) * 4 + (threadIdx.x >> 5);
+    const int jj = threadIdx.x & 31;
+    const int64_t gj = cb * BN + jj;
+    const bool ok = live && cb < CB && gj < n;
+    const double *Bb = B + b * b_stride + gj * r;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) v[t] = (ok && t < r) ? __ldg(Bb + t) : 0.0;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) mx = fmax(mx, fabs(v[t]));
+    // one exponent per 32-column tile (the tile's max |B|)
+    mx = __longlong_as_double((long long)wmax_bits((unsigned long long)__double_as_longlong(mx)));
+    const int e = scale_exp(mx);
+    if (cb >= CB) return;
+    sbq[(b * CB + cb) * BN + jj] = ok ? e : -4000;
+    const double p2 = ldexp(1.0, -e);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) v[t] *= p2;
+    base = Bq + (size_t)(b * CB + cb) * KBT * S * B_TILE;
+    boff = (jj >> 3) * 256 + (jj & 7) * 16;
+    tile_bytes = B_TILE;
+  }
+  // balanced base-128 digits, slice by slice (y <- 128 y - rint(128 y))
+  for (int s = 0; s < S; ++s) {
+    uint32_t w[KBT][2][4];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const double y = v[t] * 128.0;
+      const double q = rint(y);
+      v[t] = y - q;
+      const int kb = t / BK, h = (t % BK) / 16, kk = t % 16;
+      const uint32_t byte = ((uint32_t)(int)q & 0xffu) << (8 * (kk & 3));
+      if ((kk & 3) == 0) w[kb][h][kk >> 2] = byte;
+      else w[kb][h][kk >> 2] |= byte;
+    }
+#pragma unroll
+    for (int kb = 0; kb < KBT; ++kb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        *reinterpret_cast<uint4 *>(base + (size_t)(kb * S + s) * tile_bytes + boff + h * 128) =
+            make_uint4(w[kb][h][0], w[kb][h][1], w[kb][h][2], w[kb][h][3]);
   }
 }
 
@@ -624,8 +708,17 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
   int *sbq = sa + nb * a.m;
   sbq = reinterpret_cast<int *>(((uintptr_t)sbq + 15) & ~(uintptr_t)15);
   pf->begin("k_split", st);
-  k_split_a<<<dim3((unsigned)(4 * RB), (unsigned)nb), 64, 0, st>>>(a.A, a.m, a.r, a.a_stride, S, KB, Aq, sa, a.status);
-  k_split_b<<<dim3((unsigned)CB, (unsigned)nb), 2 * BN, 0, st>>>(a.B, a.n, a.r, a.b_stride, S, KB, Bq, sbq, a.status);
+  static const bool split_old = getenv("LRA_SPLIT_OLD") != nullptr;   // the two-kernel split (diagnostics)
+  if (split_old || KB > 2) {
+    k_split_a<<<dim3((unsigned)(4 * RB), (unsigned)nb), 64, 0, st>>>(a.A, a.m, a.r, a.a_stride, S, KB, Aq, sa, a.status);
+    k_split_b<<<dim3((unsigned)CB, (unsigned)nb), 2 * BN, 0, st>>>(a.B, a.n, a.r, a.b_stride, S, KB, Bq, sbq, a.status);
+  } else {
+    const dim3 g((unsigned)(RB + (CB + 3) / 4), (unsigned)nb);
+    if (KB == 1)
+      k_split_ab<1><<<g, 128, 0, st>>>(a.A, a.B, a.m, a.n, a.r, a.a_stride, a.b_stride, S, RB, CB, Aq, Bq, sa, sbq, a.status);
+    else
+      k_split_ab<2><<<g, 128, 0, st>>>(a.A, a.B, a.m, a.n, a.r, a.a_stride, a.b_stride, S, RB, CB, Aq, Bq, sa, sbq, a.status);
+  }
   pf->end(st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -48,48 +48,40 @@ template <typename TW, bool CPLX>
 __global__ void __launch_bounds__(SK_NT) k_sketch_structured(SketchArgs a) {
   __shared__ int64_t s_k[SK_MAXT];
   __shared__ double s_cr[SK_MAXT], s_ci[SK_MAXT];
-  __shared__ int s_T;
   const int c = blockIdx.y;
   const int64_t b = blockIdx.z;
   const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
   const int8_t *dsign = a.dsign;   // ARHT/ARFT blocks share one multiplier
-  if (threadIdx.x == 0) {
-    int T;
+  // the T signed taps of sampled column c, one thread per tap (independent loads in flight)
+  const int T = a.kind == LRA_MUL_SPARSE_PM1 ? a.nnz : (1 << a.depth);
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
     if (a.kind == LRA_MUL_SPARSE_PM1) {
-      T = a.nnz;
-      for (int t = 0; t < T; ++t) {
-        s_k[t] = a.sp_row[b * a.m_stride + (int64_t)c * a.nnz + t];
-        s_cr[t] = (double)a.sp_sign[b * a.m_stride + (int64_t)c * a.nnz + t];
-        s_ci[t] = 0.0;
-      }
+      s_k[t] = a.sp_row[b * a.m_stride + (int64_t)c * a.nnz + t];
+      s_cr[t] = (double)a.sp_sign[b * a.m_stride + (int64_t)c * a.nnz + t];
+      s_ci[t] = 0.0;
     } else {
       const int64_t sigma = a.col[c];
       const int64_t q = (int64_t)1 << a.depth, s = a.n >> a.depth;
-      T = (int)q;
-      for (int64_t t = 0; t < q; ++t) {
-        if (a.kind == LRA_MUL_ARHT) {
-          int64_t k = (sigma % s) + t * s;                       // H_{2^d} (x) I_s
-          int par = __popcll((unsigned long long)(t & (sigma / s))) & 1;
-          s_k[t] = k;
-          s_cr[t] = (double)dsign[k] * (par ? -1.0 : 1.0);
-          s_ci[t] = 0.0;
-        } else {                                                 // ARFT closed form (reading C4)
-          int64_t k = q * (sigma % s) + t;
-          int64_t e = (t * sigma) % a.n;
-          double ang = (2.0 * M_PI * (double)e) / (double)a.n;
-          double sn, cs;
-          sincos(ang, &sn, &cs);
-          double dk = (double)dsign[k];
-          s_k[t] = k;
-          s_cr[t] = dk * cs;
-          s_ci[t] = dk * sn;
-        }
+      if (a.kind == LRA_MUL_ARHT) {
+        int64_t k = (sigma % s) + t * s;                         // H_{2^d} (x) I_s
+        int par = __popcll((unsigned long long)(t & (sigma / s))) & 1;
+        s_k[t] = k;
+        s_cr[t] = (double)dsign[k] * (par ? -1.0 : 1.0);
+        s_ci[t] = 0.0;
+      } else {                                                   // ARFT closed form (reading C4)
+        int64_t k = q * (sigma % s) + t;
+        int64_t e = (t * sigma) % a.n;
+        double ang = (2.0 * M_PI * (double)e) / (double)a.n;
+        double sn, cs;
+        sincos(ang, &sn, &cs);
+        double dk = (double)dsign[k];
+        s_k[t] = k;
+        s_cr[t] = dk * cs;
+        s_ci[t] = dk * sn;
       }
     }
-    s_T = T;
   }
   __syncthreads();
-  const int T = s_T;
   const int64_t i0 = (int64_t)blockIdx.x * SK_ROWS + (int64_t)threadIdx.x * 4;
   if (i0 >= a.m) return;
   const int64_t left = a.m - i0;
