@@ -184,6 +184,34 @@ def algorithmic(name, mult, B):
     return 0, 0.0
 
 
+def ncu_traffic(kname, mats_per_launch):
+    """dram read+write bytes per launch of kname from the committed ncu --set full summary
+    (profiles/<round>/ncu_full_final.txt), scaled from that capture's problems per launch."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*",
+                                          "ncu_full_final.txt")))
+    key = {"k_ca": "k_cacl"}.get(kname, kname)
+    for path in reversed(files):
+        for line in open(path):
+            if not line.startswith("Kernel Name=") or key not in line.split(";")[0]:
+                continue
+            f = dict(kv.split("=", 1) for kv in (x.strip() for x in line.split(";")) if "=" in kv)
+            rd = float(f["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in f["dram__bytes_read.sum"] else 1e9 if "Gbyte" in f["dram__bytes_read.sum"] else 1e3)
+            wr = float(f["dram__bytes_write.sum"].split()[0]) * (1e6 if "Mbyte" in f["dram__bytes_write.sum"] else 1e9 if "Gbyte" in f["dram__bytes_write.sum"] else 1e3)
+            grid = int(re.sub(r"[^0-9]", "", f.get("launch__grid_size", "0")) or 0)
+            cdim = int(re.sub(r"[^0-9]", "", f.get("launch__cluster_dim_x", "0")) or 0)
+            if key == "k_cacl" and grid and cdim:
+                cap_mats = grid / cdim
+            elif key.startswith("k_residual"):
+                cap_mats = rd / (4096 * 4096 * 4)
+            else:
+                return None
+            return {"bytes_per_launch": (rd + wr) / cap_mats * mats_per_launch,
+                    "source": os.path.relpath(path, os.path.dirname(os.path.abspath(__file__)))}
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -287,6 +315,10 @@ def main():
         ach = byts / per_launch_s / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src, "traffic": None}
+    tr = ncu_traffic(name, per_launch_mats)
+    if tr:
+        roof["traffic"] = tr["bytes_per_launch"]
+        roof["traffic_source"] = tr["source"]
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1],
                    "share": v[0] / sum(x[0] for x in prof.values())} for k, v in prof.items()}
     stage_gbs = {}
