@@ -322,6 +322,88 @@ def expand_columns(R: np.ndarray, J, l: int, tau: float = TAU):
     return np.array(J, dtype=np.int64), scores
 
 
+def qrp_columns(R: np.ndarray, q: int, tau: float = TAU):
+    """Alg D.3 (alg1tor): greedy expansions from a vector to a k×q submatrix of the
+    k×n matrix R by Householder reflections with column pivoting.  Step g = 0..q−1:
+      1. for every column not yet chosen, the squared norm of its last k−g coordinates,
+         summed in ascending row order (one rounded product, one rounded add per term);
+      2. pivot b_g = the column of maximal norm (ties: the smallest column among the norms
+         ≥ (1 − τ)·max, reading C11);
+      3. H'_g = I − β v vᵀ with v = x + sign(x₀)‖x‖e₁, x = the pivot's last k−g coordinates,
+         β = 2 / vᵀv (vᵀv summed in ascending order): the pivot's trailing part becomes
+         −sign(x₀)‖x‖e₁ (set exactly), every other column y ← y − (β·vᵀy)·v (vᵀy summed in
+         ascending order, no fused operations);
+      4. W_{g+1} = H_g W_g.
+    The paper normalises the diagonal of R_g to 1 (reading C29: column scaling, which changes
+    neither the pivots nor the volumes' ratios; R keeps the reflected values here).
+    Returns (pivots (q,), the transformed k×n matrix H_{q−1}···H_0 R in the original column
+    order).  Raises Singular when the maximal trailing norm is 0 (rank < q)."""
+    X = np.array(R, dtype=np.float64, copy=True)
+    k, n = X.shape
+    if not 0 < q <= min(k, n):
+        raise ValueError("need 0 < q <= min(k, n)")
+    chosen = np.zeros(n, dtype=bool)
+    piv = []
+    for g in range(q):
+        nrm2 = np.zeros(n)
+        for i in range(g, k):
+            nrm2 = nrm2 + X[i, :] * X[i, :]
+        nrm2[chosen] = -1.0
+        mx = float(nrm2.max())
+        if not mx > 0.0 or not np.isfinite(mx):
+            raise Singular("rank < q in the QRP")
+        p = int(np.flatnonzero(nrm2 >= (1.0 - tau) * mx)[0])
+        x = X[g:, p].copy()
+        alpha = float(np.sqrt(nrm2[p]))
+        sgn = 1.0 if x[0] >= 0.0 else -1.0
+        v = x.copy()
+        v[0] = x[0] + sgn * alpha
+        vtv = 0.0
+        for i in range(k - g):
+            vtv = vtv + v[i] * v[i]
+        beta = 2.0 / vtv
+        w = np.zeros(n)
+        for i in range(k - g):
+            w = w + v[i] * X[g + i, :]
+        t = beta * w
+        for i in range(k - g):
+            X[g + i, :] = X[g + i, :] - t * v[i]
+        X[g:, p] = 0.0
+        X[g, p] = -sgn * alpha
+        chosen[p] = True
+        piv.append(p)
+    return np.array(piv, dtype=np.int64), X
+
+
+def projective_columns(R: np.ndarray, r: int, l: int, tau: float = TAU, tol: float = TOL):
+    """Alg 7.1 (algprjvlm): a column set J (l ≥ r columns) of the k×n matrix R
+    with maximal r-projective volume: (1) rank-revealing QRP R = QRP (Alg D.3, r steps), R′ =
+    the first r rows of the reflected matrix (r×n); (2) a maximal-volume r×l submatrix of R′:
+    the black box is maxvol (Alg D.2 stage 1 + D.1) on R′ᵀ for r columns, then Alg D.4 greedy
+    expansion to l columns.  Returns (J, piv, R′)."""
+    piv, X = qrp_columns(R, r, tau)
+    Rp = X[:r, :].copy()
+    mv = maxvol(Rp.T, None, tau, tol)
+    J = mv.S
+    if l > r:
+        J, _ = expand_columns(Rp, J, l, tau)
+    return np.asarray(J, dtype=np.int64), piv, Rp
+
+
+def cur_projective(W, mult, r: int, k: int, l: int, sweeps: int, I0=None) -> "CurResult":
+    """NEXT-3 r-projective generators: the square C-A of Alg 10.2 gives the k rows I; Alg 7.1
+    on R = W[I,:] picks l ≥ r columns of maximal r-projective volume; then the canonical
+    nucleus U = W_{k,l,r}^+ of the k×l generator, CUR = A·B and ρ."""
+    op = DenseOperand(W)
+    Y = sketch(W, mult) if mult is not None else None
+    ca = cross_approx(op, k, k, sweeps, Y=Y, I0=I0)
+    J, _, _ = projective_columns(op.rows(ca.I), r, l)
+    U, Sr, sr, Tr = canonical_nucleus(op.block(ca.I, J), r)
+    A, B = rank_r_factors(op.cols(J), op.rows(ca.I), Sr, sr, Tr)
+    num2, den2 = cur_residual(W, A, B)
+    return CurResult(ca.I, J, U, A, B, num2, den2, ca, Y)
+
+
 def cur_rectangular(W, mult, r: int, k: int, l: int, sweeps: int, I0=None) -> "CurResult":
     """k×l generators with l > k (NEXT-3): the square C-A of Alg 10.2 (k = k) gives (I, J),
     Alg D.4 expands J greedily to l columns on R = W[I,:], then the canonical nucleus

@@ -165,3 +165,78 @@ def test_rectangular_generator_exact_recovery_and_improvement():
     G5 = W[np.ix_(res.I, res.J[:5])]
     G9 = W[np.ix_(res.I, res.J)]
     assert np.linalg.det(G9 @ G9.T) >= np.linalg.det(G5 @ G5.T) * (1 - 1e-12)
+
+
+# ------------------------------------------------------------ NEXT-3: QRP (Alg D.3) and Alg 7.1
+def test_qrp_pivots_are_greedy_volume_expansions():
+    """Alg D.3: every pivot maximizes the distance of the appended column to the span of the
+    previous pivots (= the greedy expansion of Def defgrd, since v2(C|b) = v2(C)·dist(b, C)),
+    checked by least squares over all candidates; the reflected matrix keeps every column's
+    norm and the Gram matrix (orthogonal transform), is upper triangular on the pivots, and
+    its diagonal magnitudes are non-increasing."""
+    g = np.random.default_rng(21)
+    R = g.standard_normal((6, 17))
+    piv, X = lra.qrp_columns(R, 6)
+    assert len(set(piv.tolist())) == 6
+    for step in range(6):
+        prev = list(piv[:step])
+        dist = np.full(17, -1.0)
+        for j in range(17):
+            if j in prev:
+                continue
+            if prev:
+                coef = np.linalg.lstsq(R[:, prev], R[:, j], rcond=None)[0]
+                dist[j] = np.linalg.norm(R[:, j] - R[:, prev] @ coef)
+            else:
+                dist[j] = np.linalg.norm(R[:, j])
+        assert int(np.argmax(dist)) == piv[step]
+        assert abs(X[step, piv[step]]) == pytest.approx(dist[piv[step]], rel=1e-12)
+    assert np.allclose(np.linalg.norm(X, axis=0), np.linalg.norm(R, axis=0), rtol=1e-13)
+    assert np.allclose(X.T @ X, R.T @ R, atol=1e-12 * np.abs(R.T @ R).max())
+    T = X[:, piv]
+    assert np.all(np.tril(T, -1) == 0.0)
+    d = np.abs(np.diag(T))
+    assert np.all(d[:-1] >= d[1:])
+
+
+def test_qrp_rank_deficient_raises():
+    g = np.random.default_rng(22)
+    R = g.standard_normal((5, 3)) @ g.standard_normal((3, 12))
+    lra.qrp_columns(R, 3)
+    R2 = np.zeros((4, 6))
+    R2[0, 2] = 1.0
+    with pytest.raises(lra.Singular):
+        lra.qrp_columns(R2, 2)
+
+
+def test_projective_columns_volume_identity_and_brute_force():
+    """Alg 7.1 on a rank-r matrix: the r-projective volume of W[:,J] (product of its r largest
+    singular values) equals v2(R'[:,J]) (Lemma leprwnmp with the unitary Q of the QRP), and for
+    l = r the chosen set is within the factor r^(r/2) of the best r-subset (Thm thlclglb
+    through the maxvol black box), by brute force over all subsets."""
+    g = np.random.default_rng(23)
+    k, n, r = 5, 11, 3
+    W = g.standard_normal((k, r)) @ g.standard_normal((r, n))
+    for l in (3, 5):
+        J, piv, Rp = lra.projective_columns(W, r, l)
+        assert len(set(J.tolist())) == l
+        sv = np.linalg.svd(W[:, J], compute_uv=False)
+        vol_r = float(np.prod(sv[:r]))
+        vol_Rp = float(np.sqrt(np.linalg.det(Rp[:, J] @ Rp[:, J].T)))
+        assert vol_r == pytest.approx(vol_Rp, rel=1e-9)
+    J, _, _ = lra.projective_columns(W, r, r)
+    best = max(float(np.prod(np.linalg.svd(W[:, list(c)], compute_uv=False)[:r]))
+               for c in itertools.combinations(range(n), r))
+    got = float(np.prod(np.linalg.svd(W[:, J], compute_uv=False)[:r]))
+    assert got >= best / r ** (r / 2) * (1 - 1e-12)
+
+
+def test_projective_generator_exact_recovery():
+    """k×l generators of maximal r-projective volume reproduce a rank-r W up to its noise
+    (thm thcandec with the canonical nucleus) — Alg 7.1 after the square C-A (k > r needs the
+    noise: an exactly rank-r W has no nonsingular k×k generator)."""
+    W = synth.factor_gaussian(7, 160, 150, 4, 1e-20)
+    mult = synth.multiplier_abridged(7, 150, 1, 6, "arht")
+    res = lra.cur_projective(W, mult, 4, 6, 8, 2)
+    assert len(res.J) == 8 and len(set(res.J.tolist())) == 8
+    assert res.rho < 1e-8
