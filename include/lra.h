@@ -193,6 +193,28 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
    columns on entry and all l on return.  Requires k <= g0 (C full row rank), k <= 128. */
 lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t g0,
                               int64_t l, double tie_slack, void *stream);
+/* maxvol of a dense fp64 block (Alg D.2 stage 1 + Alg D.1; readings C10-C12):
+   B is N x q column-major (ld N, device, caller-owned, read only).  start == NULL: the LUP
+   cold start with the slack pivot rule, then the swap loop; start (device, q slots): the swap
+   loop from that set.  slots (device, q int64): the selected rows in slot order.  stats
+   (device, may be NULL): certificate max|C| at exit, swaps, LU steps, status (ESINGULAR on a
+   zero / non-finite pivot).  1 <= q <= min(N, 112); EINVAL otherwise.  Asynchronous. */
+lra_status lra_maxvol(lra_handle h, const double *B, int64_t N, int64_t q, const int64_t *start, double swap_tol,
+                      double tie_slack, int32_t swap_cap, int64_t *slots, lra_ca_stats *stats, void *stream);
+
+/* Greedy column expansion from a vector to k x q by Householder QR with column pivoting
+   (Alg D.3 "alg1tor"; reading C29), on R = W[I,:] (k x n; dense or entry-oracle
+   W, not row-sharded; I device, k rows).  Step g takes the column of maximal trailing norm
+   (ties: smallest column within the slack tie_slack, reading C11) and reflects the trailing
+   rows with I - beta v v^T; sums in ascending row order, no fused operations (bit-identical
+   to the oracle).  Outputs (device): piv (q pivots in order); optional R (q x n column-major,
+   ld ldr >= q) and Rt (n x q column-major): the first q rows of H_{q-1}...H_0 R in the
+   original column order — R' of Alg 7.1 when q = r.  status (device int32):
+   LRA_OK or ESINGULAR (trailing norms all zero: rank < q).  1 <= q <= min(k, n), k <= 128. */
+lra_status lra_qrp_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t q,
+                           double tie_slack, int64_t *piv, double *R, int64_t ldr, double *Rt, int32_t *status,
+                           void *stream);
+
 /* Canonical nucleus U = W_{k,l,r}^+ (Alg 3.1) of the generator W[I,J] (any k x l,
    k, l <= 128 whose Jacobi working set min(k,l)+1 columns of max(k,l) plus the rotation matrix
    fits in shared memory: square k = l <= 112; EUNSUPPORTED otherwise) and the factors A = W[:,J] T_r Sigma_r^{-1} (m x r), B = S_r^T W[I,:] (r x n),

@@ -142,6 +142,10 @@ cudaError_t launch_error_sample(const OpView &op, const double *A, const double 
                                 int64_t q, const int64_t *cols, int64_t s, double *g, double *out3, cudaStream_t st,
                                 int *nlaunch, Prof *pf);
 // NEXT-3 greedy column expansion (expand.cu); scratch: (k n + k k + n) doubles
+size_t qrp_scratch_bytes(int k, int64_t n);
+cudaError_t launch_qrp(const OpView &op, const int64_t *I, int k, int q, double tau, int64_t *piv, double *R,
+                       int64_t ldr, double *Rt, int32_t *status, void *scratch, cudaStream_t st, int *nlaunch,
+                       Prof *pf);
 cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
                                   void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,

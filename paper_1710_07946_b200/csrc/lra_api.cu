@@ -1030,6 +1030,46 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   return LRA_OK;
 }
 
+lra_status lra_maxvol(lra_handle h, const double *B, int64_t N, int64_t q, const int64_t *start, double swap_tol,
+                      double tie_slack, int32_t swap_cap, int64_t *slots, lra_ca_stats *stats, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if (!B || !slots || q < 1 || N < q || q > LRA_QMAX_ALL) return fail(LRA_EINVAL, "need 1 <= q <= min(N, %d)", LRA_QMAX_ALL);
+  if (!(swap_tol >= 0.0) || !(tie_slack >= 0.0) || tie_slack >= 1.0 || swap_cap < 0)
+    return fail(LRA_EINVAL, "bad swap_tol / tie_slack / swap_cap");
+  Carve probe{nullptr, 0};
+  probe.take<int32_t>(4);
+  probe.take<int64_t>((size_t)q);
+  probe.take<lra_ca_stats>(1);
+  if ((st = ws_reserve(h, probe.off + 256)) != LRA_OK) return st;
+  Carve cv{(char *)h->ws, 0};
+  int32_t *status = cv.take<int32_t>(4);
+  int64_t *dJ = cv.take<int64_t>((size_t)q);
+  lra_ca_stats *own = cv.take<lra_ca_stats>(1);
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t), sm));
+  return maxvol_block(h, B, N, (int)q, start, slots, swap_tol, tie_slack, swap_cap, stats ? stats : own, status, dJ, sm);
+}
+
+lra_status lra_qrp_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t q,
+                           double tie_slack, int64_t *piv, double *R, int64_t ldr, double *Rt, int32_t *status,
+                           void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "the QRP is not row-sharded");
+  if (!I || !piv || !status || k < 1 || k > 128 || q < 1 || q > k || q > W->n || !(tie_slack >= 0.0 && tie_slack < 1.0))
+    return fail(LRA_EINVAL, "need 1 <= q <= min(k, n), k <= 128");
+  if (R && ldr < q) return fail(LRA_EINVAL, "ldr < q");
+  if ((st = ws_reserve(h, qrp_scratch_bytes((int)k, W->n))) != LRA_OK) return st;
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t), sm));
+  int nl = 0;
+  CK(launch_qrp(make_view(W), I, (int)k, (int)q, tie_slack, piv, R, ldr, Rt, status, h->ws, sm, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
 // Scratch for the calls of one workload shape (reading of SURVEY 8(b) "lra_workspace_query"):
 // nb == 0 sizes lra_preprocess / lra_cross_approx / lra_cur_residual (either lra_recon) on W;
 // nb >= 1 sizes lra_batch over nb blocks shaped like W.  All four handle-owned buffers count.

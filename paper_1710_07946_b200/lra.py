@@ -86,6 +86,11 @@ def _load():
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
+    if hasattr(lib, "lra_qrp_columns"):
+        lib.lra_maxvol.argtypes = [vp, vp, i64, i64, vp, dbl, dbl, i32, vp, vp, vp]
+        lib.lra_maxvol.restype = C.c_int
+        lib.lra_qrp_columns.argtypes = [vp, P(lra_operand), vp, i64, i64, dbl, vp, vp, i64, vp, vp, vp]
+        lib.lra_qrp_columns.restype = C.c_int
     if hasattr(lib, "lra_workspace_query"):   # absent from older builds loaded through LRA_SO
         lib.lra_workspace_query.argtypes = [vp, P(lra_operand), i64, i64, i32, i64, P(C.c_size_t)]
         lib.lra_workspace_query.restype = C.c_int
@@ -123,7 +128,7 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
-            "lra_workspace_reserve"]
+            "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns"]
 
 
 def debug_counters(reset=True):
@@ -278,6 +283,23 @@ class Handle:
 
 def lra_handle_create(device=0):
     return Handle(device)
+
+
+def lra_maxvol(h, B, slots, start=None, stats=None, swap_tol=1e-12, tie_slack=1e-12, swap_cap=None, stream=None):
+    """maxvol (Alg D.2 stage 1 + D.1) of a dense fp64 block: B is a (q, N) tensor = the N x q
+    column-major block; slots (q,) int64 device."""
+    q, N = B.shape
+    cap = 20 * q if swap_cap is None else swap_cap
+    _check(lib().lra_maxvol(h.h, _ptr(B), N, q, _ptr(start), swap_tol, tie_slack, cap, _ptr(slots), _ptr(stats),
+                            _stream(stream)))
+
+
+def lra_qrp_columns(h, W, I, q, piv, status, R=None, Rt=None, tie_slack=1e-12, stream=None):
+    """Householder QRP column selection (Alg D.3) on W[I,:]: piv (q,) int64; R a (n, ldr)
+    tensor (= q x n column-major, ld ldr) or None; Rt a (q, n) tensor (= n x q column-major)."""
+    ldr = R.shape[-1] if R is not None else q
+    _check(lib().lra_qrp_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), q, tie_slack, _ptr(piv), _ptr(R), ldr,
+                                 _ptr(Rt), _ptr(status), _stream(stream)))
 
 
 def lra_workspace_query(h, W, r, k, sweeps, nb=0):

@@ -115,3 +115,35 @@ def cur_rectangular(h, W, M, r, k, l, sweeps, stream=None):
     den2 = torch.empty(1, dtype=torch.float64, device=dev)
     L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
     return bufs, J, U, A, B, num2, den2
+
+
+def cur_projective(h, W, M, r, k, l, sweeps, stream=None):
+    """k x l generators of maximal r-projective volume (NEXT-3, Alg 7.1): the square C-A of
+    Alg 10.2 gives the k rows I; on R = W[I,:] the Householder QRP (Alg D.3, r steps) gives
+    R' (r x n); maxvol of R'^T gives r columns, Alg D.4 expands them to l; then the canonical
+    nucleus / factors of the k x l generator and the a-posteriori check.
+    Returns (square bufs, J (l,), U (k, l), A, B, num2, den2, piv (r,))."""
+    cplx = M is not None and M.kind == "arft"
+    bufs = CurBuffers(W.m, W.n, r, k, cplx)
+    L.lra_preprocess(h, W, M, bufs.Y, stream=stream)
+    L.lra_cross_approx(h, W, bufs.Y, None, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.A, bufs.B, bufs.stats,
+                       y_complex=cplx, stream=stream)
+    dev = bufs.I.device
+    piv = torch.empty(r, dtype=torch.int64, device=dev)
+    status = torch.zeros(2, dtype=torch.int32, device=dev)
+    Rp = torch.empty((W.n, r), dtype=torch.float64, device=dev)      # R' (r x n column-major)
+    Rt = torch.empty((r, W.n), dtype=torch.float64, device=dev)      # R'^T (n x r column-major)
+    L.lra_qrp_columns(h, W, bufs.I, r, piv, status[0:1], R=Rp, Rt=Rt, stream=stream)
+    J = torch.empty(l, dtype=torch.int64, device=dev)
+    L.lra_maxvol(h, Rt, J[:r], stream=stream)
+    if l > r:
+        rows = torch.arange(r, dtype=torch.int64, device=dev)
+        L.lra_expand_columns(h, L.Dense(Rp), rows, J, r, stream=stream)
+    U = torch.empty((k, l), dtype=torch.float64, device=dev)
+    A = torch.empty((r, W.m), dtype=torch.float64, device=dev)
+    B = torch.empty((W.n, r), dtype=torch.float64, device=dev)
+    L.lra_nucleus_factors(h, W, bufs.I, J, r, U, A, B, status[1:2], stream=stream)
+    num2 = torch.empty(1, dtype=torch.float64, device=dev)
+    den2 = torch.empty(1, dtype=torch.float64, device=dev)
+    L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
+    return bufs, J, U, A, B, num2, den2, piv

@@ -667,3 +667,93 @@ def test_workspace_query_reserve_and_graph_capture(P, nb):
         torch.cuda.synchronize()
         assert torch.equal(eager[0], bb.I) and torch.equal(eager[1], bb.num2)
     h2.close()
+
+
+# ------------------------------------------------------------ NEXT-3: QRP (Alg D.3), maxvol, Alg 7.1
+@pytest.mark.parametrize("case", ["rand64", "cfg2_f32", "tiny_square", "ragged"])
+def test_qrp_columns_bit_exact_vs_oracle(P, h, case):
+    """Householder QRP column selection (Alg D.3) on W[I,:]: pivots and the reflected first q
+    rows are bit-identical to the oracle (same order of separately rounded operations)."""
+    g = np.random.default_rng(31)
+    if case == "rand64":
+        W = g.standard_normal((300, 700))
+        k, q = 40, 40
+    elif case == "cfg2_f32":
+        W = synth.config2(0)
+        k, q = 48, 32
+    elif case == "tiny_square":
+        W = g.standard_normal((8, 8))
+        k, q = 8, 8
+    else:
+        W = g.standard_normal((50, 1000)).astype(np.float32)
+        k, q = 13, 5
+    m, n = W.shape
+    I = g.choice(m, k, replace=False).astype(np.int64)
+    piv_o, X = O.qrp_columns(np.asarray(W, dtype=np.float64)[I, :], q)
+    It = torch.from_numpy(I).cuda()
+    piv = torch.empty(q, dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    R = torch.empty((n, q + 3), dtype=torch.float64, device="cuda")     # ld = q + 3
+    Rt = torch.empty((q, n), dtype=torch.float64, device="cuda")
+    P.lra.lra_qrp_columns(h, _dense(P, W), It, q, piv, st, R=R, Rt=Rt)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    assert list(piv.cpu().numpy()) == list(piv_o)
+    assert np.array_equal(R.cpu().numpy()[:, :q].T, X[:q, :])
+    assert np.array_equal(Rt.cpu().numpy(), X[:q, :])
+
+
+def test_qrp_rank_deficient_status(P, h):
+    g = np.random.default_rng(32)
+    W = g.standard_normal((20, 3)) @ g.standard_normal((3, 40))
+    W[:, :] = 0.0
+    It = torch.arange(5, dtype=torch.int64, device="cuda")
+    piv = torch.empty(2, dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P.lra.lra_qrp_columns(h, _dense(P, W), It, 2, piv, st)
+    torch.cuda.synchronize()
+    assert st.item() == P.lra.LRA_ESINGULAR
+
+
+@pytest.mark.parametrize("warm", [False, True])
+def test_maxvol_entry_vs_oracle(P, h, warm):
+    """lra_maxvol (Alg D.2 stage 1 + D.1 on a dense fp64 block): slots equal the oracle's,
+    cold and from a given start; dominance certificate <= 1 + tol."""
+    g = np.random.default_rng(33)
+    N, q = 1500, 20
+    B = g.standard_normal((N, q))
+    start = g.choice(N, q, replace=False).astype(np.int64) if warm else None
+    ora = O.maxvol(B, start)
+    Bt = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    slots = torch.empty(q, dtype=torch.int64, device="cuda")
+    stats = P.lra.new_stats(1, "cuda")
+    P.lra.lra_maxvol(h, Bt, slots, start=torch.from_numpy(start).cuda() if warm else None, stats=stats)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(stats)[0]
+    assert int(st["status"]) == 0
+    assert list(slots.cpu().numpy()) == list(ora.S)
+    assert float(st["cert_rows"]) <= 1 + 1e-12
+
+
+@pytest.mark.parametrize("case", ["small", "config2"])
+def test_projective_generators_vs_oracle(P, h, case):
+    """k x l generators of maximal r-projective volume (Alg 7.1 after the square C-A): QRP
+    pivots, the column set, the nucleus (1e-8) and rho (1e-4) equal the oracle's."""
+    from paper_1710_07946_b200 import pipeline
+    if case == "small":
+        W = synth.factor_gaussian(7, 600, 500, 8, 1e-12)
+        M, r, k, l = synth.multiplier_abridged(7, 500, 2, 10, "arht"), 7, 10, 12
+    else:
+        W = synth.config2(0)
+        M, r, k, l = synth.multiplier_abridged(0, 4096, 4, 48, "arht"), 32, 48, 40
+    ora = O.cur_projective(W, M, r, k, l, 3)
+    J_o, piv_o, _ = O.projective_columns(O.DenseOperand(W).rows(ora.I), r, l)
+    bufs, J, U, A, B, num2, den2, piv = pipeline.cur_projective(h, _dense(P, W), P.lra.Multiplier(M), r, k, l, 3)
+    torch.cuda.synchronize()
+    assert list(bufs.I.cpu().numpy()) == list(ora.I)
+    assert list(piv.cpu().numpy()) == list(piv_o)
+    assert list(J.cpu().numpy()) == list(ora.J)
+    Ug = U.cpu().numpy().T
+    assert np.allclose(Ug, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
+    rho = float(np.sqrt(num2.item() / den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
