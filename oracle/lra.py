@@ -322,6 +322,47 @@ def expand_columns(R: np.ndarray, J, l: int, tau: float = TAU):
     return np.array(J, dtype=np.int64), scores
 
 
+def contract_columns(R: np.ndarray, J, l: int, tau: float = TAU):
+    """Greedy contraction (Def defgrdc) of C_g = R[:, J] (k×g) down to k×l
+    (l ≥ k): each step removes the column whose removal leaves the largest volume.  Since
+    v₂(C_{g,j})² = v₂(C_g)²·(1 − c_jᵀ(C_g C_gᵀ)⁻¹c_j) (eq. eqbtr), that is the column of
+    minimal leverage ‖L⁻¹c_j‖² (L Lᵀ = C_g C_gᵀ); ties: the smallest slot with leverage ≤
+    (1 + τ)·min (reading C11).  The remaining columns keep their slot order."""
+    import scipy.linalg
+    R = np.asarray(R, dtype=np.float64)
+    J = [int(j) for j in J]
+    k = R.shape[0]
+    if l < k:
+        raise ValueError("contraction needs l >= k (C C^T nonsingular)")
+    while len(J) > l:
+        C = R[:, J]
+        L = np.linalg.cholesky(C @ C.T)
+        Z = scipy.linalg.solve_triangular(L, C, lower=True)
+        lev = np.sum(Z * Z, axis=0)
+        mn = float(lev.min())
+        t = int(np.flatnonzero(lev <= (1.0 + tau) * mn)[0])
+        del J[t]
+    return np.array(J, dtype=np.int64)
+
+
+def refine_columns(R: np.ndarray, J, cycles: int, tau: float = TAU):
+    """The expand–contract search of §scrsorth with p = 1: append the greedy
+    expansion's column (Alg D.4), then remove the greedy contraction's column (Def defgrdc);
+    stop when the contraction removes the column just appended (a fixed point), else repeat
+    (the volume never decreases: eqs. eqbun, eqbtr).  Returns (J, cycles that changed J)."""
+    J = np.asarray(J, dtype=np.int64)
+    l = len(J)
+    done = 0
+    for _ in range(cycles):
+        Jx, _ = expand_columns(R, J, l + 1, tau)
+        Jc = contract_columns(R, Jx, l, tau)
+        if list(Jc) == list(J):
+            break
+        J = Jc
+        done += 1
+    return J, done
+
+
 def qrp_columns(R: np.ndarray, q: int, tau: float = TAU):
     """Alg D.3 (alg1tor): greedy expansions from a vector to a k×q submatrix of the
     k×n matrix R by Householder reflections with column pivoting.  Step g = 0..q−1:

@@ -240,3 +240,43 @@ def test_projective_generator_exact_recovery():
     res = lra.cur_projective(W, mult, 4, 6, 8, 2)
     assert len(res.J) == 8 and len(set(res.J.tolist())) == 8
     assert res.rho < 1e-8
+
+
+def test_contract_columns_brute_force_and_identity():
+    """Greedy contraction: the removed column maximizes the remaining det(C C^T) over all
+    choices (brute force), and det drops by exactly 1 - leverage (eq. eqbtr)."""
+    g = np.random.default_rng(24)
+    R = g.standard_normal((4, 25))
+    J0 = [1, 4, 6, 9, 13, 17, 21, 24]
+    J = list(J0)
+    for target in range(7, 3, -1):
+        C = R[:, J]
+        d0 = np.linalg.det(C @ C.T)
+        dets = []
+        for t in range(len(J)):
+            Ct = R[:, J[:t] + J[t + 1:]]
+            dets.append(np.linalg.det(Ct @ Ct.T))
+        Jn = list(lra.contract_columns(R, J, target))
+        removed = [t for t in range(len(J)) if J[t] not in Jn]
+        assert len(removed) == 1 and removed[0] == int(np.argmax(dets))
+        lev = R[:, J[removed[0]]] @ np.linalg.solve(C @ C.T, R[:, J[removed[0]]])
+        assert dets[removed[0]] / d0 == pytest.approx(1 - lev, rel=1e-9)
+        assert Jn == [j for j in J if j != J[removed[0]]]      # slot order kept
+        J = Jn
+
+
+def test_refine_columns_monotone_and_fixed_point():
+    """Expand-contract cycles (p = 1): the volume never decreases, and at exit the greedy
+    expansion's column is the greedy contraction's choice (fixed point), checked by brute
+    force over all single additions and removals."""
+    g = np.random.default_rng(25)
+    R = g.standard_normal((5, 40))
+    J0 = np.array([0, 1, 2, 3, 4, 5, 6], dtype=np.int64)
+    vol = lambda J: np.linalg.det(R[:, J] @ R[:, J].T)
+    J, done = lra.refine_columns(R, J0, 50)
+    assert done >= 1 and vol(J) >= vol(J0) * (1 - 1e-12)
+    cand = [j for j in range(40) if j not in J]
+    jstar = max(cand, key=lambda j: vol(list(J) + [j]))
+    Jx = list(J) + [jstar]
+    best_removal = max(range(len(Jx)), key=lambda t: vol(Jx[:t] + Jx[t + 1:]))
+    assert Jx[best_removal] == jstar
