@@ -193,6 +193,21 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
    columns on entry and all l on return.  Requires k <= g0 (C full row rank), k <= 128. */
 lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t g0,
                               int64_t l, double tie_slack, void *stream);
+/* Greedy contraction (Def defgrdc; eq. eqbtr) of the column set of R = W[I,:]
+   (k x n): J (device) holds g0 slots on entry and its first l on return (k <= l <= g0); each
+   step removes the column of minimal leverage ||L^{-1} c_j||^2 (L L^T = C C^T), ties: the
+   smallest slot within (1 + tie_slack) min; the other slots keep their order.  Dense or
+   entry-oracle W, not row-sharded; k <= 128. */
+lra_status lra_contract_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J,
+                                int64_t g0, int64_t l, double tie_slack, void *stream);
+/* The expand-contract search of section scrsorth with p = 1: up to `cycles`
+   times append the greedy expansion's column (Alg D.4) and remove the greedy contraction's
+   column; stops on device at the fixed point (the contraction removes the appended column).
+   J (device, l slots) is refined in place; changed (device int32) = the cycles that changed J.
+   The volume of W[I,J] never decreases.  k <= l < n, k <= 128. */
+lra_status lra_refine_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t l,
+                              int32_t cycles, double tie_slack, int32_t *changed, void *stream);
+
 /* maxvol of a dense fp64 block (Alg D.2 stage 1 + Alg D.1; readings C10-C12):
    B is N x q column-major (ld N, device, caller-owned, read only).  start == NULL: the LUP
    cold start with the slack pivot rule, then the swap loop; start (device, q slots): the swap

@@ -18,8 +18,9 @@ __global__ void k_exp_gather(OpView op, const int64_t *I, int k, double *R) {
 
 // L (k x k, row-major, lower) with L L^T = C C^T, C = R[:, J[0..g)]; ok[0] = 0 if not SPD
 __global__ void __launch_bounds__(256) k_exp_chol(const double *R, int64_t n, int k, const int64_t *J, int g,
-                                                  double *L, int *ok) {
+                                                  double *L, int *ok, const int *stop) {
   extern __shared__ double Ms[];          // k x k
+  if (stop && *stop) return;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int a = e / k, b = e % k;
     double acc = 0.0;
@@ -50,8 +51,9 @@ __global__ void __launch_bounds__(256) k_exp_chol(const double *R, int64_t n, in
 
 // score[j] = ||L^{-1} R[:, j]||^2 (-1 for the columns already chosen)
 __global__ void __launch_bounds__(128) k_exp_scores(const double *R, int64_t n, int k, const double *L,
-                                                    const int64_t *J, int g, double *score) {
+                                                    const int64_t *J, int g, double *score, const int *stop) {
   extern __shared__ double Ls[];
+  if (stop && *stop) return;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) Ls[e] = L[e];
   __syncthreads();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -70,8 +72,10 @@ __global__ void __launch_bounds__(128) k_exp_scores(const double *R, int64_t n, 
 }
 
 // J[g] <- smallest j with score[j] >= (1 - tau) max
-__global__ void __launch_bounds__(1024) k_exp_pick(const double *score, int64_t n, double tau, int64_t *J, int g) {
+__global__ void __launch_bounds__(1024) k_exp_pick(const double *score, int64_t n, double tau, int64_t *J, int g,
+                                                   const int *stop) {
   __shared__ double red[32];
+  if (stop && *stop) return;
   __shared__ unsigned long long ri[32];
   double mx = -INFINITY;
   for (int64_t j = threadIdx.x; j < n; j += 1024) mx = fmax(mx, score[j]);
@@ -111,10 +115,109 @@ cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int
   cudaFuncSetAttribute(k_exp_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaFuncSetAttribute(k_exp_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   for (int g = g0; g < l && e == cudaSuccess; ++g) {
-    k_exp_chol<<<1, 256, sm, st>>>(R, op.n, k, J, g, L, ok);
-    k_exp_scores<<<(unsigned)((op.n + 127) / 128), 128, sm, st>>>(R, op.n, k, L, J, g, score);
-    k_exp_pick<<<1, 1024, 0, st>>>(score, op.n, tau, J, g);
+    k_exp_chol<<<1, 256, sm, st>>>(R, op.n, k, J, g, L, ok, nullptr);
+    k_exp_scores<<<(unsigned)((op.n + 127) / 128), 128, sm, st>>>(R, op.n, k, L, J, g, score, nullptr);
+    k_exp_pick<<<1, 1024, 0, st>>>(score, op.n, tau, J, g, nullptr);
     nl += 3;
+    e = cudaGetLastError();
+  }
+  pf->end(st);
+  *nlaunch += nl;
+  return e;
+}
+
+// ---------------------------------------------------------------- greedy contraction
+// Def defgrdc: remove from C_g = R[:, J[0..g)] the column of minimal leverage
+// ||L^{-1} c_j||^2 (L L^T = C_g C_g^T), ties: the smallest slot within (1 + tau) min; the other
+// slots keep their order.  lev[t] for the g slots (thread per slot, the k_exp_scores arithmetic).
+__global__ void __launch_bounds__(128) k_con_scores(const double *R, int64_t n, int k, const double *L,
+                                                    const int64_t *J, int g, double *lev, const int *stop) {
+  extern __shared__ double Ls[];
+  if (stop && *stop) return;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) Ls[e] = L[e];
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g) return;
+  const int64_t j = J[t];
+  double z[128];
+  double sc = 0.0;
+  for (int i = 0; i < k; ++i) {
+    double v = R[(int64_t)i * n + j];
+    for (int c = 0; c < i; ++c) v = fma(-Ls[i * k + c], z[c], v);
+    z[i] = v / Ls[i * k + i];
+    sc = fma(z[i], z[i], sc);
+  }
+  lev[t] = sc;
+}
+
+// one thread: remove the slot; in refinement mode (stop != null) removing the last slot (the
+// column just appended) is the fixed point: set *stop.
+__global__ void k_con_pick(const double *lev, int g, double tau, int64_t *J, int *stop) {
+  if (stop && *stop) return;
+  double mn = INFINITY;
+  for (int t = 0; t < g; ++t) mn = fmin(mn, lev[t]);
+  const double thr = (1.0 + tau) * mn;
+  int ts = g - 1;
+  for (int t = 0; t < g; ++t)
+    if (lev[t] <= thr) { ts = t; break; }
+  if (stop && ts == g - 1) { *stop = 1; return; }
+  for (int t = ts; t + 1 < g; ++t) J[t] = J[t + 1];
+}
+
+// count of cycles that changed J (refinement diagnostics)
+__global__ void k_con_count(const int *stop, int *changed) {
+  if (!*stop) ++*changed;
+}
+
+cudaError_t launch_contract_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
+                                    void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf) {
+  double *R = reinterpret_cast<double *>(scratch);
+  double *L = R + (size_t)k * op.n;
+  double *lev = L + (size_t)k * k;
+  pf->begin("k_contract", st);
+  k_exp_gather<<<dim3(32, (unsigned)k), 256, 0, st>>>(op, I, k, R);
+  cudaError_t e = cudaGetLastError();
+  int nl = 1;
+  const size_t sm = (size_t)k * k * 8;
+  cudaFuncSetAttribute(k_exp_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_con_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  for (int g = g0; g > l && e == cudaSuccess; --g) {
+    k_exp_chol<<<1, 256, sm, st>>>(R, op.n, k, J, g, L, ok, nullptr);
+    k_con_scores<<<(unsigned)((g + 127) / 128), 128, sm, st>>>(R, op.n, k, L, J, g, lev, nullptr);
+    k_con_pick<<<1, 1, 0, st>>>(lev, g, tau, J, nullptr);
+    nl += 3;
+    e = cudaGetLastError();
+  }
+  pf->end(st);
+  *nlaunch += nl;
+  return e;
+}
+
+// p = 1 expand-contract cycles on J (l slots; the buffer holds l + 1): stop / changed are
+// device ints (zeroed by the caller); every launch after the fixed point is a no-op.
+cudaError_t launch_refine_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int l, int cycles,
+                                  double tau, void *scratch, int *ok, int *stop, int *changed, cudaStream_t st,
+                                  int *nlaunch, Prof *pf) {
+  double *R = reinterpret_cast<double *>(scratch);
+  double *L = R + (size_t)k * op.n;
+  double *score = L + (size_t)k * k;
+  pf->begin("k_refine", st);
+  k_exp_gather<<<dim3(32, (unsigned)k), 256, 0, st>>>(op, I, k, R);
+  cudaError_t e = cudaGetLastError();
+  int nl = 1;
+  const size_t sm = (size_t)k * k * 8;
+  cudaFuncSetAttribute(k_exp_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_exp_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_con_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  for (int c = 0; c < cycles && e == cudaSuccess; ++c) {
+    k_exp_chol<<<1, 256, sm, st>>>(R, op.n, k, J, l, L, ok, stop);
+    k_exp_scores<<<(unsigned)((op.n + 127) / 128), 128, sm, st>>>(R, op.n, k, L, J, l, score, stop);
+    k_exp_pick<<<1, 1024, 0, st>>>(score, op.n, tau, J, l, stop);
+    k_exp_chol<<<1, 256, sm, st>>>(R, op.n, k, J, l + 1, L, ok, stop);
+    k_con_scores<<<(unsigned)((l + 1 + 127) / 128), 128, sm, st>>>(R, op.n, k, L, J, l + 1, score, stop);
+    k_con_pick<<<1, 1, 0, st>>>(score, l + 1, tau, J, stop);
+    k_con_count<<<1, 1, 0, st>>>(stop, changed);
+    nl += 7;
     e = cudaGetLastError();
   }
   pf->end(st);

@@ -146,6 +146,11 @@ size_t qrp_scratch_bytes(int k, int64_t n);
 cudaError_t launch_qrp(const OpView &op, const int64_t *I, int k, int q, double tau, int64_t *piv, double *R,
                        int64_t ldr, double *Rt, int32_t *status, void *scratch, cudaStream_t st, int *nlaunch,
                        Prof *pf);
+cudaError_t launch_contract_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
+                                    void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_refine_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int l, int cycles,
+                                  double tau, void *scratch, int *ok, int *stop, int *changed, cudaStream_t st,
+                                  int *nlaunch, Prof *pf);
 cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
                                   void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,

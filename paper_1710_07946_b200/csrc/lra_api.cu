@@ -828,6 +828,51 @@ lra_status lra_expand_columns(lra_handle h, const lra_operand *W, const int64_t 
   return LRA_OK;
 }
 
+lra_status lra_contract_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J,
+                                int64_t g0, int64_t l, double tie_slack, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "column contraction is not row-sharded");
+  if (!I || !J || k < 1 || k > 128 || l < k || g0 < l || g0 > W->n || !(tie_slack >= 0.0 && tie_slack < 1.0))
+    return fail(LRA_EINVAL, "need 1 <= k <= l <= g0 <= n, k <= 128");
+  const size_t base = ((size_t)k * W->n + (size_t)k * k + W->n) * 8;
+  if ((st = ws_reserve(h, base + 512)) != LRA_OK) return st;
+  int *ok = (int *)((char *)h->ws + (base + 255) / 256 * 256);
+  int nl = 0;
+  CK(launch_contract_columns(make_view(W), I, (int)k, J, (int)g0, (int)l, tie_slack, h->ws, ok, (cudaStream_t)stream,
+                             &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_refine_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t l,
+                              int32_t cycles, double tie_slack, int32_t *changed, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "column refinement is not row-sharded");
+  if (!I || !J || !changed || k < 1 || k > 128 || l < k || l + 1 > W->n || cycles < 0 ||
+      !(tie_slack >= 0.0 && tie_slack < 1.0))
+    return fail(LRA_EINVAL, "need 1 <= k <= l < n, k <= 128, cycles >= 0");
+  const size_t base = ((size_t)k * W->n + (size_t)k * k + W->n) * 8;
+  const size_t off_i = (base + 255) / 256 * 256;
+  if ((st = ws_reserve(h, off_i + 256 + (size_t)(l + 1) * 8 + 256)) != LRA_OK) return st;
+  int *ok = (int *)((char *)h->ws + off_i);
+  int *stop = ok + 1;
+  int64_t *Jw = (int64_t *)((char *)h->ws + off_i + 256);
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(stop, 0, sizeof(int), sm));
+  CK(cudaMemsetAsync(changed, 0, sizeof(int32_t), sm));
+  CK(cudaMemcpyAsync(Jw, J, (size_t)l * 8, cudaMemcpyDeviceToDevice, sm));
+  int nl = 0;
+  CK(launch_refine_columns(make_view(W), I, (int)k, Jw, (int)l, cycles, tie_slack, h->ws, ok, stop, changed, sm, &nl,
+                           &h->prof));
+  CK(cudaMemcpyAsync(J, Jw, (size_t)l * 8, cudaMemcpyDeviceToDevice, sm));
+  h->launches += nl;
+  return LRA_OK;
+}
+
 lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, int64_t k,
                                int64_t l, int64_t r, double *U, double *A, double *B, int32_t *status, void *stream) {
   lra_status st;

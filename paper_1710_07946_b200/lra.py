@@ -86,6 +86,11 @@ def _load():
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
+    if hasattr(lib, "lra_refine_columns"):
+        lib.lra_contract_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i64, dbl, vp]
+        lib.lra_contract_columns.restype = C.c_int
+        lib.lra_refine_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i32, dbl, vp, vp]
+        lib.lra_refine_columns.restype = C.c_int
     if hasattr(lib, "lra_qrp_columns"):
         lib.lra_maxvol.argtypes = [vp, vp, i64, i64, vp, dbl, dbl, i32, vp, vp, vp]
         lib.lra_maxvol.restype = C.c_int
@@ -128,7 +133,8 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
-            "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns"]
+            "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns", "lra_contract_columns",
+            "lra_refine_columns"]
 
 
 def debug_counters(reset=True):
@@ -344,6 +350,18 @@ def lra_expand_columns(h, W, I, J, g0, tie_slack=1e-12, stream=None):
     """J (l,) int64 device tensor: first g0 entries given, the rest filled greedily (Alg D.4)."""
     _check(lib().lra_expand_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), _ptr(J), g0, J.numel(), tie_slack,
                                     _stream(stream)))
+
+
+def lra_contract_columns(h, W, I, J, l, tie_slack=1e-12, stream=None):
+    """J (g0,) int64 device tensor: on return its first l entries are the contracted set."""
+    _check(lib().lra_contract_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), _ptr(J), J.numel(), l, tie_slack,
+                                      _stream(stream)))
+
+
+def lra_refine_columns(h, W, I, J, cycles, changed, tie_slack=1e-12, stream=None):
+    """J (l,) int64 device tensor refined in place by expand-contract cycles; changed (1,) int32."""
+    _check(lib().lra_refine_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), _ptr(J), J.numel(), int(cycles),
+                                    tie_slack, _ptr(changed), _stream(stream)))
 
 
 def lra_nucleus_factors(h, W, I, J, r, U, A, B, status, stream=None):

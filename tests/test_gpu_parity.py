@@ -757,3 +757,33 @@ def test_projective_generators_vs_oracle(P, h, case):
     assert np.allclose(Ug, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
     rho = float(np.sqrt(num2.item() / den2.item()))
     assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
+
+
+@pytest.mark.parametrize("case", ["rand64", "cfg2_f32"])
+def test_contract_and_refine_columns_vs_oracle(P, h, case):
+    """Greedy contraction (Def defgrdc) and the p = 1 expand-contract refinement on W[I,:]:
+    the column sets (slot order) and the number of changing cycles equal the oracle's."""
+    g = np.random.default_rng(41)
+    if case == "rand64":
+        W = g.standard_normal((300, 500))
+        k, g0, l = 8, 30, 12
+    else:
+        W = synth.config2(0)
+        k, g0, l = 16, 60, 24
+    m, n = W.shape
+    I = g.choice(m, k, replace=False).astype(np.int64)
+    J0 = g.choice(n, g0, replace=False).astype(np.int64)
+    R = np.asarray(W, dtype=np.float64)[I, :]
+    Jc_o = O.contract_columns(R, J0, l)
+    Jr_o, done_o = O.refine_columns(R, Jc_o, 40)
+    It = torch.from_numpy(I).cuda()
+    J = torch.from_numpy(J0.copy()).cuda()
+    P.lra.lra_contract_columns(h, _dense(P, W), It, J, l)
+    torch.cuda.synchronize()
+    assert list(J.cpu().numpy()[:l]) == list(Jc_o)
+    Jr = J[:l].clone()
+    changed = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P.lra.lra_refine_columns(h, _dense(P, W), It, Jr, 40, changed)
+    torch.cuda.synchronize()
+    assert list(Jr.cpu().numpy()) == list(Jr_o)
+    assert changed.item() == done_o
