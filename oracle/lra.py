@@ -36,6 +36,8 @@ def sketch(W: np.ndarray, mult: dict) -> np.ndarray:
     W = np.asarray(W, dtype=np.float64)
     m, n = W.shape
     kind, lbar = mult["kind"], mult["lbar"]
+    if kind == "qgauss":                      # NEXT-4: Y = W·Ω with Ω = G_q[:, σ] (exact integers)
+        return sketch(W, dict(kind="gaussian", lbar=lbar, omega=qgauss_omega(mult), n=mult["n"]))
     if kind == "arht":
         Y = np.zeros((m, lbar))
         for c, sig in enumerate(mult["col"]):
@@ -69,6 +71,29 @@ def sketch(W: np.ndarray, mult: dict) -> np.ndarray:
             Y = Y + np.outer(W[:, k], Om[k, :])
         return Y
     raise ValueError(kind)
+
+
+def bidiag_product_columns(perm, diag, sub, col) -> np.ndarray:
+    """Columns `col` of G = M_0 M_1 ... M_{q-1}, M_i = B_i P_i (def11 / def2):
+    B_i has diag[i][c] at (c, c) and sub[i][c] at (c + 1 mod n, c); P_i[perm[i][c], c] = 1.
+    Applied right to left to the selection S (G S = M_0 (M_1 (... (M_{q-1} S)))):
+    (P V)[perm[c]] = V[c], then (B U)[r] = diag[r] U[r] + sub[r-1] U[r-1] (cyclic).
+    Exact for integer entries below 2^53."""
+    q, n = np.asarray(perm).shape
+    V = np.zeros((n, len(col)))
+    V[np.asarray(col), np.arange(len(col))] = 1.0
+    for i in reversed(range(q)):
+        U = np.empty_like(V)
+        U[np.asarray(perm[i]), :] = V
+        V = np.asarray(diag[i], dtype=np.float64)[:, None] * U + np.roll(np.asarray(sub[i], dtype=np.float64)[:, None] * U, 1, axis=0)
+    return V
+
+
+def qgauss_omega(mult: dict) -> np.ndarray:
+    """Ω = G_q[:, σ] of the quasi-Gaussian multiplier (ones on the diagonal, random signs on
+    the cyclic subdiagonal, NEXT-4); the sketch is then Y = W·Ω as for a Gaussian Ω."""
+    q, n = mult["qg_perm"].shape
+    return bidiag_product_columns(mult["qg_perm"], np.ones((q, n)), mult["qg_sign"], mult["col"])
 
 
 def preprocess_full(W: np.ndarray, mult: dict) -> np.ndarray:

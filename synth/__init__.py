@@ -193,6 +193,20 @@ def multiplier_gaussian(seed: int, n: int, lbar: int, round_fp32: bool = True) -
     return dict(kind="gaussian", depth=0, lbar=int(lbar), omega=np.asfortranarray(om), n=int(n))
 
 
+def multiplier_qgauss(seed: int, n: int, q: int, lbar: int) -> dict:
+    """Quasi-Gaussian multiplier (NEXT-4, section sqsgss / sgpbd, def11):
+    G_q = M_0 M_1 ... M_{q-1} with M_i = B_i P_i, B_i the cyclic bidiagonal matrix with ones on
+    the diagonal and random signs s_i[c] at (c + 1 mod n, c) (the corner is c = n - 1), P_i a
+    uniform random permutation with P_i[perm_i[c], c] = 1; then lbar sampled columns (the
+    first lbar of a uniform permutation, reading C30).  Arrays: sign (q, n) int8, perm (q, n)
+    int64, col (lbar,)."""
+    g = rng(seed, S_MULT)
+    sign = (g.integers(0, 2, size=(q, n)) * 2 - 1).astype(np.int8)
+    perm = np.stack([g.permutation(n) for _ in range(q)]).astype(np.int64)
+    col = g.permutation(n)[:lbar].astype(np.int64)
+    return dict(kind="qgauss", depth=int(q), lbar=int(lbar), qg_sign=sign, qg_perm=perm, col=col, n=int(n))
+
+
 def random_rows(seed: int, m: int, k: int) -> np.ndarray:
     """k distinct uniform row indices (Tests 2 random start I₀)."""
     return rng(seed, S_I0).permutation(m)[:k].astype(np.int64)
