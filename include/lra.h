@@ -71,7 +71,12 @@ typedef enum {
   LRA_MUL_GAUSSIAN = 1,  /* omega: n x lbar fp64 column-major (ld_omega)                       */
   LRA_MUL_ARHT = 2,      /* (D H_{n,d} P)[:, col]: dsign[n] in {+1,-1}, col[lbar], 2^depth | n  */
   LRA_MUL_ARFT = 3,      /* (D Omega_{n,d} P)[:, col]; Y is complex128                         */
-  LRA_MUL_SPARSE_PM1 = 4 /* column c: rows sp_row[c*nnz+t], signs sp_sign[c*nnz+t], t < nnz    */
+  LRA_MUL_SPARSE_PM1 = 4,/* column c: rows sp_row[c*nnz+t], signs sp_sign[c*nnz+t], t < nnz    */
+  LRA_MUL_QGAUSS = 5     /* quasi-Gaussian (def11; reading C30): G = M_0...M_{q-1},
+                            M_i = B_i P_i, q = depth (1..30); B_i: ones on the diagonal, qg_sign
+                            [i*n + c] at (c+1 mod n, c); P_i[qg_perm[i*n + c], c] = 1; the sketch
+                            uses the lbar columns col of G (built exactly on the device, then
+                            applied like a Gaussian omega)                                   */
 } lra_mul_kind;
 
 typedef struct {
@@ -85,6 +90,8 @@ typedef struct {
   int32_t nnz_per_col;
   const double *omega;      /* GAUSSIAN                              */
   int64_t ld_omega;
+  const int8_t *qg_sign;    /* QGAUSS: depth x n subdiagonal signs   */
+  const int64_t *qg_perm;   /* QGAUSS: depth x n permutations        */
 } lra_multiplier;
 
 typedef struct lra_handle_s *lra_handle;

@@ -151,6 +151,8 @@ cudaError_t launch_contract_columns(const OpView &op, const int64_t *I, int k, i
 cudaError_t launch_refine_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int l, int cycles,
                                   double tau, void *scratch, int *ok, int *stop, int *changed, cudaStream_t st,
                                   int *nlaunch, Prof *pf);
+cudaError_t launch_qg_build(int64_t n, int q, int64_t lbar, const int8_t *sign, const int64_t *perm,
+                            const int64_t *col, int *work, double *omega, cudaStream_t st, Prof *pf);
 cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
                                   void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,

@@ -87,6 +87,8 @@ struct lra_handle_s {
   size_t gm_bytes;
   void *sh;                       // row-sharded path: assembled blocks
   size_t sh_bytes;
+  void *qg;                       // quasi-Gaussian multiplier: built omega + integer work
+  size_t qg_bytes;
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -206,6 +208,10 @@ static lra_status check_mult(const lra_multiplier *M, int64_t n) {
     case LRA_MUL_GAUSSIAN:
       if (!M->omega || M->ld_omega < n) return fail(LRA_EINVAL, "gaussian multiplier needs omega, ld >= n");
       return LRA_OK;
+    case LRA_MUL_QGAUSS:
+      if (M->depth < 1 || M->depth > 30 || !M->qg_sign || !M->qg_perm || !M->col)
+        return fail(LRA_EINVAL, "quasi-Gaussian multiplier needs 1 <= depth <= 30, qg_sign, qg_perm, col");
+      return LRA_OK;
     default:
       return fail(LRA_EINVAL, "bad multiplier kind");
   }
@@ -229,6 +235,26 @@ static SketchArgs make_sketch(const lra_operand *W, const lra_multiplier *M, voi
   a.sp_sign = M->sp_sign;
   a.y = Y;
   return a;
+}
+
+// A quasi-Gaussian multiplier is realized as its lbar sampled columns Omega = G_q[:, col]
+// (exact integers, built on the device into the handle's qg buffer) and then applied exactly
+// like a Gaussian omega; every other kind passes through unchanged.
+static lra_status resolve_mult(lra_handle h, const lra_multiplier *M, int64_t n, cudaStream_t st,
+                               lra_multiplier *out) {
+  *out = *M;
+  if (M->kind != LRA_MUL_QGAUSS) return LRA_OK;
+  const size_t need = (size_t)n * M->lbar * (8 + 2 * 4) + 256;
+  lra_status s;
+  if ((s = buf_reserve(&h->qg, &h->qg_bytes, need, "the quasi-Gaussian multiplier")) != LRA_OK) return s;
+  double *omega = (double *)h->qg;
+  int *work = (int *)(omega + (size_t)n * M->lbar);
+  CK(launch_qg_build(n, M->depth, M->lbar, M->qg_sign, M->qg_perm, M->col, work, omega, st, &h->prof));
+  h->launches += 1;
+  out->kind = LRA_MUL_GAUSSIAN;
+  out->omega = omega;
+  out->ld_omega = n;
+  return LRA_OK;
 }
 
 // Reconstruction path of the full residual: fp32 W (or FAST) -> tensor-core
@@ -309,6 +335,7 @@ void lra_handle_destroy(lra_handle h) {
   if (h->gs) cudaFree(h->gs);
   if (h->gm) cudaFree(h->gm);
   if (h->sh) cudaFree(h->sh);
+  if (h->qg) cudaFree(h->qg);
   if (h->comm) nccl().CommDestroy(h->comm);
   for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
   if (h->streams_ready) {
@@ -377,8 +404,10 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multipli
   if (W->kind != LRA_OP_DENSE) return fail(LRA_EINVAL, "lra_preprocess needs a dense operand");
   if ((s = check_mult(M, W->n)) != LRA_OK) return s;
   if (!Y || ldy < W->m) return fail(LRA_EINVAL, "Y null or ldy < m");
-  SketchArgs a = make_sketch(W, M, Y, ldy);
-  CK(launch_sketch(a, 1, M->omega, M->ld_omega, (cudaStream_t)stream, &h->prof));
+  lra_multiplier Mr;
+  if ((s = resolve_mult(h, M, W->n, (cudaStream_t)stream, &Mr)) != LRA_OK) return s;
+  SketchArgs a = make_sketch(W, &Mr, Y, ldy);
+  CK(launch_sketch(a, 1, Mr.omega, Mr.ld_omega, (cudaStream_t)stream, &h->prof));
   h->launches += 1;
   return LRA_OK;
 }
@@ -1020,6 +1049,9 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   }
   const int64_t gsz = (nb + ngroups - 1) / ngroups;
   ngroups = (nb + gsz - 1) / gsz;
+  lra_multiplier Mres;
+  if ((s = resolve_mult(h, M0, n, st, &Mres)) != LRA_OK) return s;
+  M0 = &Mres;
   CK(cudaEventRecord(h->fork, st));
   for (int i = 0; i < LRA_NSIDE; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));
   const size_t wsz = W0->dtype == LRA_F32 ? 4 : 8;

@@ -11,6 +11,8 @@
 // with 16-byte vector loads; the kernel is HBM-bound.
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace lra {
 
 constexpr int SK_NT = 256;
@@ -146,62 +148,160 @@ __global__ void __launch_bounds__(SK_NT) k_sketch_structured(SketchArgs a) {
 // output in fp64.  When a K-chunk of Omega holds only fp32-representable values and W is
 // fp32, every product is exact and FMA equals multiply-then-add; otherwise the product is
 // rounded first (oracle order).  grid: (ceil(m/32), ceil(lbar/16), nb)
-constexpr int GS_R = 32, GS_C = 16, GS_K = 64;
-template <typename TW>
-__global__ void __launch_bounds__(128) k_sketch_gauss(SketchArgs a, const double *omega, int64_t ldo) {
-  __shared__ double Ws[GS_K][GS_R + 1];
-  __shared__ double Os[GS_K][GS_C];
-  __shared__ int s_exact;
-  const int64_t b = blockIdx.z;
+// Gaussian (and quasi-Gaussian) sketch Y = W * Omega, every output accumulated over k in
+// ascending order (the oracle's order).  One warp per CTA computes a 32-row x 16-column tile,
+// 4 x 4 outputs per lane (16 independent accumulators); W and Omega are staged through shared
+// memory 32 k at a time while the next chunk's loads are already in flight (register
+// prefetch).  When a product is exact in fp64 (fp32 W times an fp32-representable Omega — the
+// fp32-rounded Gaussian and the integer quasi-Gaussian multipliers) one DFMA equals the
+// oracle's rounded product + rounded sum; otherwise the two roundings are kept.
+// Gaussian (and quasi-Gaussian) sketch Y = W * Omega, every output accumulated over k in
+// ascending order (the oracle's order, so no split over k: the m x lbar outputs are the only
+// parallelism, ~196k chains of 4096 DFMAs for config 2).  One CTA (4 warps) owns a 16-row
+// tile and all lbar columns; thread (rg, cg) accumulates rows 2 rg, 2 rg + 1 x columns
+// cg + 16 t (t < CT), i.e. 2 CT independent chains, so the grid has ~7 warps per SM and every
+// SM sub-partition stays busy.  Per k a thread reads one 8-byte W pair and CT Omega values
+// (broadcast within its column group) from shared memory.  32-k chunks: W by a 3-stage
+// cp.async ring, Omega (column-major in global, k-major in shared memory) by register
+// prefetch one chunk ahead.  When a product is exact in fp64 (fp32 W times an
+// fp32-representable Omega — the fp32-rounded Gaussian and the integer quasi-Gaussian
+// multipliers) one DFMA equals the oracle's rounded product + rounded sum; otherwise the two
+// roundings are kept.
+constexpr int GS_K = 32, GS_R = 16, GS_ST = 3, GS_NT = 128;
+
+__device__ __forceinline__ void cpa16(void *dst, const void *src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
+template <typename TW, int CT>
+__global__ void __launch_bounds__(GS_NT) k_sketch_gauss(SketchArgs a, const double *omega, int64_t ldo) {
+  constexpr int LBP = 16 * CT;                                   // padded columns
+  constexpr int NO = GS_K * LBP / GS_NT;                         // Omega values per thread per chunk
+  constexpr int ST = GS_ST;
+  __shared__ __align__(16) TW Wst[ST][GS_K][GS_R];
+  __shared__ __align__(16) double Os[GS_K][LBP + 1];
+  const int64_t b = blockIdx.y;
   const TW *W = reinterpret_cast<const TW *>(a.w) + b * a.w_stride;
-  const int64_t r0 = (int64_t)blockIdx.x * GS_R, c0 = (int64_t)blockIdx.y * GS_C;
-  const int tid = threadIdx.x;
-  const int tr = tid % 16, tc = tid / 16;     // thread: rows tr, tr+16; cols tc, tc+8
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  const bool wf32 = sizeof(TW) == 4;
-  for (int64_t k0 = 0; k0 < a.n; k0 += GS_K) {
-    int exact = 1;
-    for (int e = tid; e < GS_K * GS_R; e += 128) {
-      int kk = e / GS_R, rr = e % GS_R;
-      int64_t i = r0 + rr, k = k0 + kk;
-      Ws[kk][rr] = (i < a.m && k < a.n) ? (double)W[k * a.ldw + i] : 0.0;
-    }
-    for (int e = tid; e < GS_K * GS_C; e += 128) {
-      int kk = e / GS_C, cc = e % GS_C;
-      int64_t k = k0 + kk, c = c0 + cc;
-      double o = (k < a.n && c < a.lbar) ? omega[c * ldo + k] : 0.0;
-      Os[kk][cc] = o;
-      exact &= ((double)(float)o == o);
-    }
-    exact = __syncthreads_and(exact && wf32);
-    const int kmax = (int)min((int64_t)GS_K, a.n - k0);
-    if (exact) {
-      for (int kk = 0; kk < kmax; ++kk) {
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-          for (int y = 0; y < 2; ++y) acc[x][y] = fma(Ws[kk][tr + 16 * x], Os[kk][tc + 8 * y], acc[x][y]);
+  const int64_t r0 = (int64_t)blockIdx.x * GS_R;
+  const int tid = threadIdx.x, rg = tid & 7, cg = tid >> 3;
+  const int64_t nchunk = (a.n + GS_K - 1) / GS_K;
+  const bool wvec = ((a.ldw * (int64_t)sizeof(TW)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0) &&
+                    r0 + GS_R <= a.m;
+  auto load_w = [&](int64_t ch, int stg) {
+    const int64_t k0 = ch * GS_K;
+    constexpr int WPER = 16 / (int)sizeof(TW);
+    if (wvec) {
+      for (int e = tid; e < GS_K * GS_R / WPER; e += GS_NT) {
+        const int kk = e / (GS_R / WPER), rr = (e % (GS_R / WPER)) * WPER;
+        const int64_t k = k0 + kk;
+        cpa16(&Wst[stg][kk][rr], W + (k < a.n ? k : 0) * a.ldw + r0 + rr, k < a.n ? 16 : 0);
       }
     } else {
-      for (int kk = 0; kk < kmax; ++kk) {
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-          for (int y = 0; y < 2; ++y)
-            acc[x][y] = __dadd_rn(acc[x][y], __dmul_rn(Ws[kk][tr + 16 * x], Os[kk][tc + 8 * y]));
+      for (int e = tid; e < GS_K * GS_R; e += GS_NT) {
+        const int kk = e / GS_R, rr = e % GS_R;
+        const int64_t k = k0 + kk, i = r0 + rr;
+        Wst[stg][kk][rr] = (k < a.n && i < a.m) ? W[k * a.ldw + i] : (TW)0;
       }
     }
+  };
+  double opre[NO];
+  auto load_o = [&](int64_t ch) {
+    const int64_t k0 = ch * GS_K;
+#pragma unroll
+    for (int t = 0; t < NO; ++t) {
+      const int e = tid + GS_NT * t, kk = e % GS_K, c = e / GS_K;
+      const int64_t k = k0 + kk;
+      opre[t] = (c < a.lbar && k < a.n) ? __ldg(omega + (int64_t)c * ldo + k) : 0.0;
+    }
+  };
+  double acc[2][CT];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < CT; ++y) acc[x][y] = 0.0;
+  for (int p = 0; p < ST - 1; ++p) {
+    if (p < nchunk) load_w(p, p);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  load_o(0);
+  for (int64_t ch = 0; ch < nchunk; ++ch) {
+    if (ch + ST - 1 < nchunk) load_w(ch + ST - 1, (int)((ch + ST - 1) % ST));
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    int ex = sizeof(TW) == 4;
+#pragma unroll
+    for (int t = 0; t < NO; ++t) {
+      const int e = tid + GS_NT * t;
+      Os[e % GS_K][e / GS_K] = opre[t];
+      ex &= ((double)(float)opre[t] == opre[t]);
+    }
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 1) : "memory");
+    const bool exact = __syncthreads_and(ex);          // also publishes Os and this stage of W
+    if (ch + 1 < nchunk) load_o(ch + 1);               // in flight during the chunk
+    const int stg = (int)(ch % ST);
+    const int kmax = (int)min((int64_t)GS_K, a.n - ch * GS_K);
+#define GS_BODY(OPR)                                                                             \
+  {                                                                                             \
+    const double w0 = (double)Wst[stg][kk][2 * rg], w1 = (double)Wst[stg][kk][2 * rg + 1];      \
+    _Pragma("unroll") for (int y = 0; y < CT; ++y) {                                            \
+      const double o = Os[kk][cg + 16 * y];                                                     \
+      acc[0][y] = OPR(w0, o, acc[0][y]);                                                        \
+      acc[1][y] = OPR(w1, o, acc[1][y]);                                                        \
+    }                                                                                           \
+  }
+#define GS_FMA(w, o, c) fma(w, o, c)
+#define GS_RND(w, o, c) __dadd_rn(c, __dmul_rn(w, o))
+    if (exact) {
+      if (kmax == GS_K) {
+#pragma unroll 8
+        for (int kk = 0; kk < GS_K; ++kk) GS_BODY(GS_FMA)
+      } else {
+        for (int kk = 0; kk < kmax; ++kk) GS_BODY(GS_FMA)
+      }
+    } else {
+      if (kmax == GS_K) {
+#pragma unroll 8
+        for (int kk = 0; kk < GS_K; ++kk) GS_BODY(GS_RND)
+      } else {
+        for (int kk = 0; kk < kmax; ++kk) GS_BODY(GS_RND)
+      }
+    }
+#undef GS_BODY
+#undef GS_FMA
+#undef GS_RND
     __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   double *Y = reinterpret_cast<double *>(a.y) + b * a.y_stride;
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
-    for (int y = 0; y < 2; ++y) {
-      int64_t i = r0 + tr + 16 * x, c = c0 + tc + 8 * y;
+    for (int y = 0; y < CT; ++y) {
+      const int64_t i = r0 + 2 * rg + x, c = cg + 16 * y;
       if (i < a.m && c < a.lbar) Y[c * a.ldy + i] = acc[x][y];
     }
-  (void)s_exact;
+}
+
+template <typename TW, int CT>
+static cudaError_t launch_gauss_t(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st) {
+  dim3 grid((unsigned)((a.m + GS_R - 1) / GS_R), (unsigned)nb);
+  k_sketch_gauss<TW, CT><<<grid, GS_NT, 0, st>>>(a, omega, ldo);
+  return cudaGetLastError();
+}
+
+template <typename TW>
+static cudaError_t launch_gauss(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st) {
+  switch ((a.lbar + 15) / 16) {
+    case 1: return launch_gauss_t<TW, 1>(a, nb, omega, ldo, st);
+    case 2: return launch_gauss_t<TW, 2>(a, nb, omega, ldo, st);
+    case 3: return launch_gauss_t<TW, 3>(a, nb, omega, ldo, st);
+    case 4: return launch_gauss_t<TW, 4>(a, nb, omega, ldo, st);
+    case 5: return launch_gauss_t<TW, 5>(a, nb, omega, ldo, st);
+    case 6: return launch_gauss_t<TW, 6>(a, nb, omega, ldo, st);
+    case 7: return launch_gauss_t<TW, 7>(a, nb, omega, ldo, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ---------------------------------------------------------------- NEXT-1: all n columns
@@ -275,12 +375,11 @@ cudaError_t launch_transform_full(const SketchArgs &a, int *pinv, void *out, int
 cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo,
                           cudaStream_t st, Prof *pf) {
   if (a.kind == LRA_MUL_GAUSSIAN) {
-    dim3 grid((unsigned)((a.m + GS_R - 1) / GS_R), (unsigned)((a.lbar + GS_C - 1) / GS_C), (unsigned)nb);
     pf->begin("k_sketch_gauss", st);
-    if (a.dtype == LRA_F32) k_sketch_gauss<float><<<grid, 128, 0, st>>>(a, omega, ldo);
-    else k_sketch_gauss<double><<<grid, 128, 0, st>>>(a, omega, ldo);
+    const cudaError_t e = a.dtype == LRA_F32 ? launch_gauss<float>(a, nb, omega, ldo, st)
+                                             : launch_gauss<double>(a, nb, omega, ldo, st);
     pf->end(st);
-    return cudaGetLastError();
+    return e;
   }
   dim3 grid((unsigned)((a.m + SK_ROWS - 1) / SK_ROWS), (unsigned)a.lbar, (unsigned)nb);
   const bool cplx = a.kind == LRA_MUL_ARFT;
@@ -292,6 +391,47 @@ cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, 
     if (cplx) k_sketch_structured<double, true><<<grid, SK_NT, 0, st>>>(a);
     else k_sketch_structured<double, false><<<grid, SK_NT, 0, st>>>(a);
   }
+  pf->end(st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- quasi-Gaussian multiplier
+// Omega = G_q[:, col], G_q = M_0 ... M_{q-1}, M_i = B_i P_i (def11; reading C30):
+// one CTA per sampled column c, the column vector in global scratch (two int32 buffers of n;
+// entries are integers with |.| <= 2^q, q <= 30), the factors applied right to left:
+//   U = P_i V:  U[perm_i[j]] = V[j];   V = B_i U:  V[r] = U[r] + sign_i[r-1] U[r-1]  (cyclic).
+__global__ void __launch_bounds__(1024) k_qg_build(int64_t n, int q, const int8_t *sign, const int64_t *perm,
+                                                   const int64_t *col, int *work, double *omega) {
+  extern __shared__ int qsm[];                       // 2 n ints when they fit (else global work)
+  const int64_t c = blockIdx.x;
+  int *V = work ? work + (size_t)c * 2 * n : qsm, *U = V + n;
+  const int64_t sc = col[c];
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) V[j] = j == sc ? 1 : 0;
+  __syncthreads();
+  for (int i = q - 1; i >= 0; --i) {
+    const int64_t *pi = perm + (size_t)i * n;
+    const int8_t *si = sign + (size_t)i * n;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) U[pi[j]] = V[j];
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
+      const int64_t rm = r == 0 ? n - 1 : r - 1;
+      V[r] = U[r] + (int)si[rm] * U[rm];
+    }
+    __syncthreads();
+  }
+  for (int64_t r = threadIdx.x; r < n; r += blockDim.x) omega[(size_t)c * n + r] = (double)V[r];
+}
+
+cudaError_t launch_qg_build(int64_t n, int q, int64_t lbar, const int8_t *sign, const int64_t *perm,
+                            const int64_t *col, int *work, double *omega, cudaStream_t st, Prof *pf) {
+  pf->begin("k_qg_build", st);
+  const size_t smem = (size_t)2 * n * sizeof(int);
+  const bool in_smem = smem <= 200 * 1024;
+  if (in_smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_qg_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_qg_build<<<(unsigned)lbar, 1024, in_smem ? smem : 0, st>>>(n, q, sign, perm, col, in_smem ? nullptr : work, omega);
   pf->end(st);
   return cudaGetLastError();
 }

@@ -23,10 +23,10 @@ _SO = os.environ.get("LRA_SO") or os.path.join(_HERE, "liblra.so")   # LRA_SO: d
 LRA_OK, LRA_EINVAL, LRA_ESINGULAR, LRA_ENOMEM, LRA_ECUDA, LRA_ENCCL, LRA_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 LRA_F32, LRA_F64 = 0, 1
 LRA_OP_DENSE, LRA_OP_FACTORED_CSR = 0, 1
-LRA_MUL_NONE, LRA_MUL_GAUSSIAN, LRA_MUL_ARHT, LRA_MUL_ARFT, LRA_MUL_SPARSE_PM1 = 0, 1, 2, 3, 4
+LRA_MUL_NONE, LRA_MUL_GAUSSIAN, LRA_MUL_ARHT, LRA_MUL_ARFT, LRA_MUL_SPARSE_PM1, LRA_MUL_QGAUSS = 0, 1, 2, 3, 4, 5
 LRA_RECON_FAST, LRA_RECON_PRECISE = 0, 1
 MUL_KIND = {"none": LRA_MUL_NONE, "gaussian": LRA_MUL_GAUSSIAN, "arht": LRA_MUL_ARHT,
-            "arft": LRA_MUL_ARFT, "sparse": LRA_MUL_SPARSE_PM1}
+            "arft": LRA_MUL_ARFT, "sparse": LRA_MUL_SPARSE_PM1, "qgauss": LRA_MUL_QGAUSS}
 
 
 class lra_operand(C.Structure):
@@ -39,7 +39,8 @@ class lra_operand(C.Structure):
 class lra_multiplier(C.Structure):
     _fields_ = [("kind", C.c_int32), ("depth", C.c_int32), ("lbar", C.c_int64), ("dsign", C.c_void_p),
                 ("col", C.c_void_p), ("sp_row", C.c_void_p), ("sp_sign", C.c_void_p),
-                ("nnz_per_col", C.c_int32), ("omega", C.c_void_p), ("ld_omega", C.c_int64)]
+                ("nnz_per_col", C.c_int32), ("omega", C.c_void_p), ("ld_omega", C.c_int64),
+                ("qg_sign", C.c_void_p), ("qg_perm", C.c_void_p)]
 
 
 STATS_DTYPE = np.dtype([("status", np.int32), ("loops_done", np.int32), ("lu_steps", np.int32),
@@ -218,7 +219,7 @@ class Multiplier:
         self.mult = mult
         self.kind = mult["kind"]
         self.t = {}
-        for key in ("dsign", "col", "sp_row", "sp_sign"):
+        for key in ("dsign", "col", "sp_row", "sp_sign", "qg_sign", "qg_perm"):
             if key in mult:
                 self.t[key] = torch.from_numpy(np.ascontiguousarray(mult[key])).to(device)
         if "omega" in mult:   # (lbar, n) storage of the n×lbar col-major matrix
@@ -231,7 +232,8 @@ class Multiplier:
         return lra_multiplier(MUL_KIND[self.kind], int(self.mult.get("depth", 0)), self.lbar,
                               _ptr(self.t.get("dsign")), _ptr(self.t.get("col")), _ptr(self.t.get("sp_row")),
                               _ptr(self.t.get("sp_sign")), int(self.mult.get("nnz", 0)), _ptr(om),
-                              self.n if om is not None else 0)
+                              self.n if om is not None else 0, _ptr(self.t.get("qg_sign")),
+                              _ptr(self.t.get("qg_perm")))
 
     def m_stride(self):
         """Per-block stride for lra_batch: stacked sparse multipliers (synth.multiplier_sparse_batch)

@@ -787,3 +787,40 @@ def test_contract_and_refine_columns_vs_oracle(P, h, case):
     torch.cuda.synchronize()
     assert list(Jr.cpu().numpy()) == list(Jr_o)
     assert changed.item() == done_o
+
+
+# ------------------------------------------------------------ NEXT-4: quasi-Gaussian multipliers
+@pytest.mark.parametrize("q", [1, 20])
+def test_config2_qgauss_vs_oracle(P, h, q):
+    """Config 2 sketched with a quasi-Gaussian multiplier (q random cyclic bidiagonal and
+    permutation factors, def11): the device-built omega is exact, so Y is bit-identical; the
+    pivots, loops, swaps, U and rho (1e-4) equal the oracle's."""
+    W = synth.config2(0)
+    M = synth.multiplier_qgauss(0, 4096, q, 48)
+    _check_pipeline(P, h, W, M, 32, 48, 3, rho_tol_rel=1e-4, y_exact=True)
+
+
+def test_config1_qgauss_fp64(P, h):
+    """Config 1 (fp64) with q = 12 factors: exact recovery and bit-exact pivots."""
+    W = synth.config1(0)
+    M = synth.multiplier_qgauss(1, 256, 12, 8)
+    rho, _ = _check_pipeline(P, h, W, M, 8, 8, 2, rho_tol_abs=1e-12, y_exact=False)
+    assert rho <= 1e-9
+
+
+def test_config3_batch_qgauss_vs_oracle(P, h):
+    """lra_batch with one quasi-Gaussian multiplier shared by 16 Cauchy blocks (built once per
+    call): every block's pivots equal the oracle's, rho within 1e-4."""
+    from paper_1710_07946_b200 import pipeline
+    nb = 16
+    s, t = synth.cauchy_params(0, nb)
+    Wt = synth.cauchy_blocks_torch(s, t, "cuda")
+    Mq = synth.multiplier_qgauss(3, 512, 10, 20)
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), P.lra.Multiplier(Mq), 16, 20, 2, nb)
+    torch.cuda.synchronize()
+    for b in range(nb):
+        ora = O.cur_pipeline(synth.cauchy_block(s[b], t[b]), Mq, 16, 20, 20, 2)
+        assert list(bufs.I[b].cpu().numpy()) == list(ora.I)
+        assert list(bufs.J[b].cpu().numpy()) == list(ora.J)
+        rho = float(np.sqrt(bufs.num2[b].item() / bufs.den2[b].item()))
+        assert abs(rho / ora.rho - 1) <= 1e-4, (b, rho, ora.rho)
