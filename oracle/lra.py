@@ -388,6 +388,50 @@ def refine_columns(R: np.ndarray, J, cycles: int, tau: float = TAU):
     return J, done
 
 
+def leverage_scores(B: np.ndarray, r: int) -> np.ndarray:
+    """SVD-based leverage scores of the n columns of the k×n matrix B (eq. eqlevsc with β = 1,
+    eq. eqlevsc1): p_j = ‖(V_r)_{j,:}‖² / r with V_r the r top right singular
+    vectors (numpy's SVD as the library step).  Σ p_j = 1."""
+    B = np.asarray(B, dtype=np.float64)
+    _, sv, Vt = np.linalg.svd(B, full_matrices=False)
+    if not 0 < r <= len(sv) or not sv[r - 1] > 0.0:
+        raise Singular("leverage scores need rank >= r")
+    V = Vt[:r, :].T
+    return np.sum(V * V, axis=1) / r
+
+
+def sample_exactly(p: np.ndarray, l: int, u: np.ndarray):
+    """Alg C.1 (algsmplex, "Exactly(l)"): l independent picks with
+    Probability(i_t = i) = p_i and the rescaling d_t = 1/sqrt(l·p_{i_t}).  The random picks are
+    the caller's uniforms u_t ∈ [0, 1) through the inverse CDF: i_t = the smallest i with
+    u_t·P_{n-1} < P_i, P_i = p_0 + … + p_i summed sequentially (reading C31)."""
+    p = np.asarray(p, dtype=np.float64)
+    P = np.cumsum(p)
+    idx = np.searchsorted(P, np.asarray(u, dtype=np.float64) * P[-1], side="right").astype(np.int64)
+    idx = np.minimum(idx, len(p) - 1)
+    return idx, 1.0 / np.sqrt(l * p[idx])
+
+
+def cur_leverage(W, r: int, k: int, l: int, sweeps: int, I0, uniforms) -> "CurResult":
+    """C-A iterations with the leverage-score sampling of DMM08 (stages 1–2 of Alg 9.1
+    "algcurlevsc", with Alg C.1) as the subalgorithm of every horizontal and
+    vertical step (§ststc-alvrg): from the rows I0, sweep s samples l columns from
+    the leverage scores of W[I,:] with uniforms[2s] and then k rows from those of W[:,J]ᵀ with
+    uniforms[2s+1]; the nucleus is the canonical U = W_{I,J,r}⁺ (Remark resmplfc's unscaled
+    form, reading C31), CUR = A·B and ρ."""
+    W = np.asarray(W)
+    op = DenseOperand(W)
+    I = np.asarray(I0, dtype=np.int64)
+    J = None
+    for s in range(sweeps):
+        J, _ = sample_exactly(leverage_scores(op.rows(I), r), l, uniforms[2 * s])
+        I, _ = sample_exactly(leverage_scores(op.cols(J).T, r), k, uniforms[2 * s + 1])
+    U, Sr, sr, Tr = canonical_nucleus(op.block(I, J), r)
+    A, B = rank_r_factors(op.cols(J), op.rows(I), Sr, sr, Tr)
+    num2, den2 = cur_residual(W, A, B)
+    return CurResult(I, J, U, A, B, num2, den2, None, None)
+
+
 def qrp_columns(R: np.ndarray, q: int, tau: float = TAU):
     """Alg D.3 (alg1tor): greedy expansions from a vector to a k×q submatrix of the
     k×n matrix R by Householder reflections with column pivoting.  Step g = 0..q−1:

@@ -207,6 +207,17 @@ def multiplier_qgauss(seed: int, n: int, q: int, lbar: int) -> dict:
     return dict(kind="qgauss", depth=int(q), lbar=int(lbar), qg_sign=sign, qg_perm=perm, col=col, n=int(n))
 
 
+def leverage_uniforms(seed: int, sweeps: int, k: int, l: int):
+    """The uniforms of the leverage-score sampling (Alg C.1) of cur_leverage: for sweep s,
+    (l,) for the columns then (k,) for the rows, in [0, 1)."""
+    g = rng(seed, S_MULT + 7)
+    out = []
+    for _ in range(sweeps):
+        out.append(g.random(l))
+        out.append(g.random(k))
+    return out
+
+
 def random_rows(seed: int, m: int, k: int) -> np.ndarray:
     """k distinct uniform row indices (Tests 2 random start I₀)."""
     return rng(seed, S_I0).permutation(m)[:k].astype(np.int64)
