@@ -215,6 +215,23 @@ lra_status lra_contract_columns(lra_handle h, const lra_operand *W, const int64_
 lra_status lra_refine_columns(lra_handle h, const lra_operand *W, const int64_t *I, int64_t k, int64_t *J, int64_t l,
                               int32_t cycles, double tie_slack, int32_t *changed, void *stream);
 
+/* SVD-based leverage scores (eq. eqlevsc with beta = 1, eq. eqlevsc1) of the N
+   columns of the k x N block B: side 0 -> B = W[idx,:] (N = n, column scores), side 1 ->
+   B = W[:,idx]^T (N = m, row scores).  p (device, N fp64): p_j = ||(V_r)_{j,:}||^2 / r with
+   V_r the r top right singular vectors (computed from the eigenpairs of B B^T by the Jacobi
+   nucleus kernel); sum p = 1 up to rounding.  status (device int32): LRA_OK or ESINGULAR
+   (rank of B < r).  1 <= r <= k <= 112; dense or entry-oracle W, not row-sharded. */
+lra_status lra_leverage_scores(lra_handle h, const lra_operand *W, const int64_t *idx, int64_t k, int32_t side,
+                               int64_t r, double *p, int32_t *status, void *stream);
+/* Exactly(l) sampling and rescaling (Alg C.1 "algsmplex"; reading C31): l picks
+   with Probability(i_t = i) = p_i driven by the caller's uniforms u (device, l values in
+   [0, 1)): i_t = the smallest i with u_t P_{N-1} < P_i, P the sequential prefix sums of p.
+   idx (device, l int64) gets the picks (with replacement), dscale (device, l fp64, may be
+   NULL) the rescaling 1 / sqrt(l p_{i_t}).  status (device, may be NULL): nothing is done
+   when it is not LRA_OK (chained after lra_leverage_scores). */
+lra_status lra_sample_exactly(lra_handle h, const double *p, int64_t N, int64_t l, const double *u, int64_t *idx,
+                              double *dscale, const int32_t *status, void *stream);
+
 /* maxvol of a dense fp64 block (Alg D.2 stage 1 + Alg D.1; readings C10-C12):
    B is N x q column-major (ld N, device, caller-owned, read only).  start == NULL: the LUP
    cold start with the slack pivot rule, then the swap loop; start (device, q slots): the swap

@@ -153,6 +153,11 @@ cudaError_t launch_refine_columns(const OpView &op, const int64_t *I, int k, int
                                   int *nlaunch, Prof *pf);
 cudaError_t launch_qg_build(int64_t n, int q, int64_t lbar, const int8_t *sign, const int64_t *perm,
                             const int64_t *col, int *work, double *omega, cudaStream_t st, Prof *pf);
+size_t leverage_scratch_bytes(int k, int r, int64_t N);
+cudaError_t launch_leverage_scores(const OpView &op, const int64_t *I, int k, int side, int r, double *p,
+                                   int32_t *status, void *scratch, cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_sample_exactly(const double *p, int64_t N, int l, const double *u, double *P, int64_t *idx,
+                                  double *dsc, const int32_t *status, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
                                   void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,

@@ -1107,6 +1107,38 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   return LRA_OK;
 }
 
+lra_status lra_leverage_scores(lra_handle h, const lra_operand *W, const int64_t *idx, int64_t k, int32_t side,
+                               int64_t r, double *p, int32_t *status, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (W->m_global > 0) return fail(LRA_EUNSUPPORTED, "leverage scores are not row-sharded");
+  if (!idx || !p || !status || (side != 0 && side != 1) || k < 1 || k > 112 || r < 1 || r > k ||
+      (size_t)2 * k * r * 8 > 200 * 1024)
+    return fail(LRA_EINVAL, "need side 0/1, 1 <= r <= k <= 112");
+  const int64_t N = side ? W->m : W->n;
+  if ((st = ws_reserve(h, leverage_scratch_bytes((int)k, (int)r, N))) != LRA_OK) return st;
+  cudaStream_t sm = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int32_t), sm));
+  int nl = 0;
+  CK(launch_leverage_scores(make_view(W), idx, (int)k, side, (int)r, p, status, h->ws, sm, &nl, &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_sample_exactly(lra_handle h, const double *p, int64_t N, int64_t l, const double *u, int64_t *idx,
+                              double *dscale, const int32_t *status, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if (!p || !u || !idx || N < 1 || l < 1) return fail(LRA_EINVAL, "need p, u, idx, N >= 1, l >= 1");
+  if ((st = ws_reserve(h, (size_t)N * 8 + 256)) != LRA_OK) return st;
+  int nl = 0;
+  CK(launch_sample_exactly(p, N, (int)l, u, (double *)h->ws, idx, dscale, status, (cudaStream_t)stream, &nl,
+                           &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
 lra_status lra_maxvol(lra_handle h, const double *B, int64_t N, int64_t q, const int64_t *start, double swap_tol,
                       double tie_slack, int32_t swap_cap, int64_t *slots, lra_ca_stats *stats, void *stream) {
   lra_status st;

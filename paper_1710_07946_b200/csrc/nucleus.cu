@@ -112,8 +112,11 @@ __global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
           if (ga * ga > eps2 * al * be && ga != 0.0) {
             const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
             const double z2 = fma(zeta, zeta, 1.0);
-            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused
-            const double t = copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta);
+            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused;
+            // t -> 1 / (2 zeta) once zeta^2 overflows, t = 0 for a non-finite zeta (degenerate pairs:
+            // a column at rounding level, ga below the reciprocal's range)
+            const double t = z2 < INFINITY ? copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta)
+                                           : (isfinite(zeta) ? 0.5 / zeta : 0.0);
             const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
   #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -195,8 +198,11 @@ __global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
           if (act && ga * ga > eps2 * al * be && ga != 0.0) {
             const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
             const double z2 = fma(zeta, zeta, 1.0);
-            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused
-            const double t = copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta);
+            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused;
+            // t -> 1 / (2 zeta) once zeta^2 overflows, t = 0 for a non-finite zeta (degenerate pairs:
+            // a column at rounding level, ga below the reciprocal's range)
+            const double t = z2 < INFINITY ? copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta)
+                                           : (isfinite(zeta) ? 0.5 / zeta : 0.0);
             const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -399,6 +405,10 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   kern<<<(unsigned)nb, nt, smem, st>>>(na);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!fa.A && !fa.B) {           // nucleus only (TS, Sr for the caller)
+    *nlaunch += 1;
+    return cudaSuccess;
+  }
   dim3 gA((unsigned)((fa.op.m + 127) / 128), (unsigned)nb);
   const size_t sA = (size_t)fa.l * fa.r * 8, sB = (size_t)fa.k * fa.r * 8;
   void (*kA)(FacArgs) = fa.r <= 16 ? k_factor_A<16> : (fa.r <= 32 ? k_factor_A<32> : k_factor_A<64>);

@@ -87,6 +87,11 @@ def _load():
     lib.lra_cur_certificate.restype = C.c_int
     lib.lra_variance_bound.argtypes = [dbl, i64, dbl, P(C.c_double)]
     lib.lra_variance_bound.restype = C.c_int
+    if hasattr(lib, "lra_leverage_scores"):
+        lib.lra_leverage_scores.argtypes = [vp, P(lra_operand), vp, i64, i32, i64, vp, vp, vp]
+        lib.lra_leverage_scores.restype = C.c_int
+        lib.lra_sample_exactly.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp, vp]
+        lib.lra_sample_exactly.restype = C.c_int
     if hasattr(lib, "lra_refine_columns"):
         lib.lra_contract_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i64, dbl, vp]
         lib.lra_contract_columns.restype = C.c_int
@@ -135,7 +140,7 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
             "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns", "lra_contract_columns",
-            "lra_refine_columns"]
+            "lra_refine_columns", "lra_leverage_scores", "lra_sample_exactly"]
 
 
 def debug_counters(reset=True):
@@ -352,6 +357,18 @@ def lra_expand_columns(h, W, I, J, g0, tie_slack=1e-12, stream=None):
     """J (l,) int64 device tensor: first g0 entries given, the rest filled greedily (Alg D.4)."""
     _check(lib().lra_expand_columns(h.h, C.byref(W.struct()), _ptr(I), I.numel(), _ptr(J), g0, J.numel(), tie_slack,
                                     _stream(stream)))
+
+
+def lra_leverage_scores(h, W, idx, side, r, p, status, stream=None):
+    """Leverage scores of the columns of W[idx,:] (side 0) or of the rows of W[:,idx] (side 1)."""
+    _check(lib().lra_leverage_scores(h.h, C.byref(W.struct()), _ptr(idx), idx.numel(), int(side), int(r), _ptr(p),
+                                     _ptr(status), _stream(stream)))
+
+
+def lra_sample_exactly(h, p, u, idx, dscale=None, status=None, stream=None):
+    """Alg C.1: idx (l,) int64 picks from p (N,) with the uniforms u (l,)."""
+    _check(lib().lra_sample_exactly(h.h, _ptr(p), p.numel(), idx.numel(), _ptr(u), _ptr(idx), _ptr(dscale),
+                                    _ptr(status), _stream(stream)))
 
 
 def lra_contract_columns(h, W, I, J, l, tie_slack=1e-12, stream=None):

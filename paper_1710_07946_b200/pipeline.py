@@ -147,3 +147,31 @@ def cur_projective(h, W, M, r, k, l, sweeps, stream=None):
     den2 = torch.empty(1, dtype=torch.float64, device=dev)
     L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
     return bufs, J, U, A, B, num2, den2, piv
+
+
+def cur_leverage(h, W, r, k, l, sweeps, I0, uniforms, stream=None):
+    """C-A iterations with DMM08's leverage-score sampling as the subalgorithm (NEXT-4; Alg 9.1
+    stages 1-2 with Alg C.1 in every horizontal and vertical step, section ststc-alvrg): from
+    the rows I0, each sweep samples l columns from the leverage scores of W[I,:] and k rows from
+    those of W[:,J]^T with the given uniforms (device tensors: uniforms[2s] (l,), [2s+1] (k,));
+    then the canonical nucleus / factors and the a-posteriori check.
+    Returns (I, J, U (k, l), A, B, num2, den2, status (3,))."""
+    dev = I0.device
+    I = I0.clone()
+    J = torch.empty(l, dtype=torch.int64, device=dev)
+    pc = torch.empty(W.n, dtype=torch.float64, device=dev)
+    pr = torch.empty(W.m, dtype=torch.float64, device=dev)
+    status = torch.zeros(3, dtype=torch.int32, device=dev)
+    for s in range(sweeps):
+        L.lra_leverage_scores(h, W, I, 0, r, pc, status[0:1], stream=stream)
+        L.lra_sample_exactly(h, pc, uniforms[2 * s], J, status=status[0:1], stream=stream)
+        L.lra_leverage_scores(h, W, J, 1, r, pr, status[1:2], stream=stream)
+        L.lra_sample_exactly(h, pr, uniforms[2 * s + 1], I, status=status[1:2], stream=stream)
+    U = torch.empty((k, l), dtype=torch.float64, device=dev)
+    A = torch.empty((r, W.m), dtype=torch.float64, device=dev)
+    B = torch.empty((W.n, r), dtype=torch.float64, device=dev)
+    L.lra_nucleus_factors(h, W, I, J, r, U, A, B, status[2:3], stream=stream)
+    num2 = torch.empty(1, dtype=torch.float64, device=dev)
+    den2 = torch.empty(1, dtype=torch.float64, device=dev)
+    L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
+    return I, J, U, A, B, num2, den2, status

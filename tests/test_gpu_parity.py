@@ -824,3 +824,62 @@ def test_config3_batch_qgauss_vs_oracle(P, h):
         assert list(bufs.J[b].cpu().numpy()) == list(ora.J)
         rho = float(np.sqrt(bufs.num2[b].item() / bufs.den2[b].item()))
         assert abs(rho / ora.rho - 1) <= 1e-4, (b, rho, ora.rho)
+
+
+# ------------------------------------------------------------ NEXT-4: leverage-score C-A (DMM08)
+@pytest.mark.parametrize("side", [0, 1])
+def test_leverage_scores_vs_oracle(P, h, side):
+    """SVD-based leverage scores (eq. eqlevsc, beta = 1) of the columns of W[I,:] / rows of
+    W[:,J] on config 2 (k = 48, r = 32) match the oracle's SVD-based values to 1e-9."""
+    g = np.random.default_rng(61)
+    W = synth.config2(0)
+    idx = g.choice(4096, 48, replace=False).astype(np.int64)
+    Wd = np.asarray(W, dtype=np.float64)
+    B = Wd[idx, :] if side == 0 else Wd[:, idx].T
+    p_o = O.leverage_scores(B, 32)
+    p = torch.empty(4096, dtype=torch.float64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P.lra.lra_leverage_scores(h, _dense(P, W), torch.from_numpy(idx).cuda(), side, 32, p, st)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    assert np.allclose(p.cpu().numpy(), p_o, rtol=1e-9, atol=1e-12 * p_o.max())
+
+
+def test_sample_exactly_vs_oracle(P, h):
+    g = np.random.default_rng(62)
+    p = g.random(5000)
+    p /= p.sum()
+    u = g.random(300)
+    idx_o, d_o = O.sample_exactly(p, 300, u)
+    idx = torch.empty(300, dtype=torch.int64, device="cuda")
+    d = torch.empty(300, dtype=torch.float64, device="cuda")
+    P.lra.lra_sample_exactly(h, torch.from_numpy(p).cuda(), torch.from_numpy(u).cuda(), idx, dscale=d)
+    torch.cuda.synchronize()
+    assert list(idx.cpu().numpy()) == list(idx_o)
+    assert np.allclose(d.cpu().numpy(), d_o, rtol=1e-15)
+
+
+@pytest.mark.parametrize("case", ["small", "config2"])
+def test_cur_leverage_vs_oracle(P, h, case):
+    """Leverage-score C-A (DMM08's Alg 1 as the subalgorithm, Alg C.1 sampling with the same
+    uniforms): the sampled row and column sequences equal the oracle's, U to 1e-8, rho 1e-4."""
+    from paper_1710_07946_b200 import pipeline
+    if case == "small":
+        W = synth.factor_gaussian(9, 300, 260, 5, 1e-16)
+        r, k, l, sw = 5, 15, 15, 2
+    else:
+        W = synth.config2(0)
+        r, k, l, sw = 32, 48, 48, 2
+    m, n = W.shape
+    I0 = synth.random_rows(9, m, k)
+    uni = synth.leverage_uniforms(9, sw, k, l)
+    ora = O.cur_leverage(W, r, k, l, sw, I0, uni)
+    I, J, U, A, B, num2, den2, st = pipeline.cur_leverage(
+        h, _dense(P, W), r, k, l, sw, torch.from_numpy(I0).cuda(), [torch.from_numpy(x).cuda() for x in uni])
+    torch.cuda.synchronize()
+    assert list(st.cpu().numpy()) == [0, 0, 0]
+    assert list(I.cpu().numpy()) == list(ora.I)
+    assert list(J.cpu().numpy()) == list(ora.J)
+    assert np.allclose(U.cpu().numpy().T, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
+    rho = float(np.sqrt(num2.item() / den2.item()))
+    assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
