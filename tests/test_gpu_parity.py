@@ -883,3 +883,36 @@ def test_cur_leverage_vs_oracle(P, h, case):
     assert np.allclose(U.cpu().numpy().T, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
     rho = float(np.sqrt(num2.item() / den2.item()))
     assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
+
+
+def test_new_entry_points_reject_bad_arguments(P, h):
+    """The NEXT-3/4 entry points fail loudly (EINVAL / EUNSUPPORTED) instead of computing on
+    bad shapes."""
+    L = P.lra
+    W = synth.config1(0)
+    Wd = _dense(P, W)
+    I = torch.arange(8, dtype=torch.int64, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with pytest.raises(L.LraError) as e:
+        L.lra_qrp_columns(h, Wd, I, 9, torch.empty(9, dtype=torch.int64, device="cuda"), st)
+    assert e.value.status == L.LRA_EINVAL
+    with pytest.raises(L.LraError) as e:
+        L.lra_maxvol(h, torch.zeros((20, 10), dtype=torch.float64, device="cuda"),
+                     torch.empty(20, dtype=torch.int64, device="cuda"))
+    assert e.value.status == L.LRA_EINVAL
+    with pytest.raises(L.LraError) as e:
+        L.lra_leverage_scores(h, Wd, I, 0, 9, torch.empty(256, dtype=torch.float64, device="cuda"), st)
+    assert e.value.status == L.LRA_EINVAL
+    with pytest.raises(L.LraError) as e:
+        L.lra_contract_columns(h, Wd, I, torch.arange(12, dtype=torch.int64, device="cuda"), 5)
+    assert e.value.status == L.LRA_EINVAL
+    big = torch.arange(120, dtype=torch.int64, device="cuda")
+    with pytest.raises(L.LraError) as e:
+        L.lra_nucleus_factors(h, Wd, big, big, 100, torch.empty((120, 120), dtype=torch.float64, device="cuda"),
+                              torch.empty((100, 256), dtype=torch.float64, device="cuda"),
+                              torch.empty((256, 100), dtype=torch.float64, device="cuda"), st)
+    assert e.value.status == L.LRA_EUNSUPPORTED
+    M = synth.multiplier_qgauss(0, 256, 31, 8)
+    with pytest.raises(L.LraError) as e:
+        L.lra_preprocess(h, Wd, L.Multiplier(M), torch.empty((8, 256), dtype=torch.float64, device="cuda"))
+    assert e.value.status == L.LRA_EINVAL
