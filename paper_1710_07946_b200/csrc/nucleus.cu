@@ -35,7 +35,7 @@ __device__ __forceinline__ void rr_pair(int L, int round, int i, int &a, int &b)
 // the xor-16 and xor-8 butterfly levels, then finishes with xor 4, 2, 1 — the same sums in the
 // same association, so every rotation, and the whole SVD, is unchanged while a round issues a
 // quarter of the warps (the round was fp64-issue-bound with one warp per pair).
-template <int KU, bool OLD, int PL>
+template <int KU, bool OLD, int PL, int KC = 0>
 __global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
   const int NT = blockDim.x, NW = NT >> 5;
   extern __shared__ __align__(16) double nsm[];
@@ -45,8 +45,9 @@ __global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
   // A wide generator (k < l, NEXT-3 rectangular case) is handled through its transpose so
   // that Jacobi always orthogonalises the shorter dimension: H = G^T = S' Sigma V^T gives
   // G = V Sigma S'^T, i.e. S = V and T = S' (columns of the rotated H over sigma).
-  const bool tr = a.k < a.l;
-  const int k = tr ? a.l : a.k, l = tr ? a.k : a.l;   // H is k x l, k >= l
+  const bool tr = KC ? false : a.k < a.l;
+  // KC > 0: a square KC x KC generator known at compile time (constant-folded bounds)
+  const int k = KC ? KC : (tr ? a.l : a.k), l = KC ? KC : (tr ? a.k : a.l);   // H is k x l, k >= l
   const int L = (l + 1) & ~1;          // even number of columns (zero pad)
   const int ldg = k;                   // H column stride
   double *G = nsm;                     // L columns of length k
@@ -388,6 +389,21 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
       {k_nucleus<1, false, 32>, k_nucleus<2, false, 32>, k_nucleus<3, false, 32>, k_nucleus<4, false, 32>}};
   const int row = old ? 0 : (PLs == 8 ? 1 : PLs == 16 ? 2 : 3);
   KF kern = tab[row][ku - 1];
+  static const bool generic = getenv("LRA_NUC_GENERIC") != nullptr;   // diagnostics
+  static const int kcpl = getenv("LRA_NUC_KCPL") ? atoi(getenv("LRA_NUC_KCPL")) : 16;   // diagnostics
+  int PLk = PLs;
+  if (!old && !generic && pl_env == 0 && na.k == na.l) {   // square shapes of the BASELINE configs
+    if (na.k == 48) {
+      PLk = kcpl;
+      kern = kcpl == 8 ? k_nucleus<2, false, 8, 48> : kcpl == 32 ? k_nucleus<2, false, 32, 48> : k_nucleus<2, false, 16, 48>;
+    } else if (na.k == 20) {
+      kern = k_nucleus<1, false, 16, 20>;
+    } else if (na.k == 8) {
+      kern = k_nucleus<1, false, 16, 8>;
+    } else if (na.k == 96) {
+      kern = k_nucleus<3, false, 32, 96>;
+    }
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   pf->begin("k_nucleus", st);
@@ -397,7 +413,7 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
     nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
     if (nt > 1024) nt = 1024;
   } else {
-    const int gpw = 32 / PLs;               // pairs per warp
+    const int gpw = 32 / PLk;               // pairs per warp
     nt = ((L / 2 + gpw - 1) / gpw) * 32;
     if (nt < 256) nt = 256;
     if (nt > 512) nt = 512;                 // the pair loop strides over the rest
