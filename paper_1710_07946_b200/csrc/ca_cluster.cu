@@ -382,7 +382,7 @@ __device__ __forceinline__ void mm_part(Kx<Q> &k, int q, double *out, const doub
 
 // Steps: 0 = stage 2 on a real sketch Y (cold); then 2L+1 = horizontal step of loop L
 // (J <- maxvol(W[I,:]^T), cold in loop 0), 2L+2 = vertical step (I <- maxvol(W[:,J]), warm).
-template <int Q, int TPR, int OPK>
+template <int Q, int TPR, int OPK, bool QEQ = false>
 __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
   constexpr int W = Q / TPR, QP = Q | 1;
   static_assert(W % 2 == 0 || W == 1, "W even");
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
   k.par = 0;
   k.tau = a.tau;
   const double tol = a.tol;
-  const int q = a.q;
+  const int q = QEQ ? Q : a.q;           // QEQ: q == Q known at compile time (loops fold)
   const int64_t b = blockIdx.x / a.cs;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
@@ -715,8 +715,10 @@ static cudaError_t launch_cc_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   a.rpc = rpc;
   a.grid = 0;
   if (cs_out) *cs_out = cs;
-  void (*kern)(CAArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? ccl::k_cacl<Q, TPR, 2>
-                         : (a.op.dtype == LRA_F64 ? ccl::k_cacl<Q, TPR, 1> : ccl::k_cacl<Q, TPR, 0>);
+  const bool qeq = a.q == Q;
+  void (*kern)(CAArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? (qeq ? ccl::k_cacl<Q, TPR, 2, true> : ccl::k_cacl<Q, TPR, 2>)
+                         : (a.op.dtype == LRA_F64 ? (qeq ? ccl::k_cacl<Q, TPR, 1, true> : ccl::k_cacl<Q, TPR, 1>)
+                                                  : (qeq ? ccl::k_cacl<Q, TPR, 0, true> : ccl::k_cacl<Q, TPR, 0>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (cs > 8) {
