@@ -290,7 +290,7 @@ __device__ __forceinline__ unsigned decide_exact(Sh<Q> &sh, unsigned mine, const
   return sh.didx;
 }
 
-template <int Q, int TPR, int OPK>
+template <int Q, int TPR, int OPK, bool QEQ = false>
 __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
   constexpr int W = Q / TPR, RPP = NT / TPR;
   static_assert(W % 2 == 0, "W even");
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
   __shared__ Sh<Q> sh;
   const int tid = threadIdx.x, lane = tid & 31;
   const int sub = tid % TPR, jb = sub * W, gl = lane & ~(TPR - 1);
-  const int q = a.q;
+  const int q = QEQ ? Q : a.q;           // QEQ: q == Q known at compile time
   const double tau = a.tau, tol = a.tol;
   OpView op = a.op;
   int par = 0;
@@ -620,8 +620,10 @@ static cudaError_t launch_gm_t(CAArgs a, int64_t nb, int64_t maxN, void *scratch
   g.gx = reinterpret_cast<unsigned *>(p);
   p += 2 * 160 * 4;
   g.inS = reinterpret_cast<unsigned char *>(p);
-  void (*kern)(CAArgs, GmArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? k_cagm<Q, TPR, 2>
-                                 : (a.op.dtype == LRA_F64 ? k_cagm<Q, TPR, 1> : k_cagm<Q, TPR, 0>);
+  const bool qeq = a.q == Q;
+  void (*kern)(CAArgs, GmArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? (qeq ? k_cagm<Q, TPR, 2, true> : k_cagm<Q, TPR, 2>)
+                                 : (a.op.dtype == LRA_F64 ? (qeq ? k_cagm<Q, TPR, 1, true> : k_cagm<Q, TPR, 1>)
+                                                          : (qeq ? k_cagm<Q, TPR, 0, true> : k_cagm<Q, TPR, 0>));
   const size_t smem = (size_t)Q * Q * 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
