@@ -297,81 +297,128 @@ size_t nucleus_smem(int k, int l) {
 // A = W[:,J] * TS: one thread per row of A computes all r outputs (accumulated in ascending j,
 // as before), the l gathered values W[i, J[j]] loaded 16 at a time (coalesced across rows).
 // grid (ceil(m/128), nb), 128 threads.  r <= 64 (registers: r doubles per thread).
-template <int RMAX>
+// The coefficient matrix (TS for A, Sr for B) sits in shared memory transposed, c[j][u]
+// (RMAX columns, zero beyond r), so one 16-byte load feeds two outputs; each thread owns RR
+// rows of A (columns of B) that share those loads.  Every output is the same fma chain over
+// j (s) ascending as before, so A and B are bit-identical to the one-row version.
+template <int RMAX, int RR>
 __global__ void __launch_bounds__(128) k_factor_A(FacArgs a) {
-  extern __shared__ double ts[];          // l x r: ts[t * l + j]
+  extern __shared__ __align__(16) double ts[];   // l x RMAX: ts[j * RMAX + u]
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int l = a.l, r = a.r;
   const double *TS = a.TS + b * (int64_t)l * r;
-  for (int e = threadIdx.x; e < l * r; e += 128) ts[e] = TS[e];
+  for (int e = threadIdx.x; e < l * RMAX; e += 128) {
+    const int j = e / RMAX, u = e % RMAX;
+    ts[e] = u < r ? TS[u * l + j] : 0.0;
+  }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  if (i >= op.m) return;
+  const int64_t i0 = (int64_t)blockIdx.x * (128 * RR) + threadIdx.x;
+  if (i0 >= op.m) return;
   const int64_t *J = a.J + b * l;
-  double acc[RMAX];
+  double acc[RR][RMAX];
 #pragma unroll
-  for (int u = 0; u < RMAX; ++u) acc[u] = 0.0;
-  for (int j0 = 0; j0 < l; j0 += 16) {
-    double w[16];
+  for (int x = 0; x < RR; ++x)
 #pragma unroll
-    for (int x = 0; x < 16; ++x) w[x] = (j0 + x < l) ? op.at(i, J[j0 + x]) : 0.0;
+    for (int u = 0; u < RMAX; ++u) acc[x][u] = 0.0;
+  constexpr int PF = 8;
+  for (int j0 = 0; j0 < l; j0 += PF) {
+    double w[RR][PF];
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      if (j0 + x < l) {
+    for (int x = 0; x < RR; ++x)
 #pragma unroll
-        for (int u = 0; u < RMAX; ++u)
-          if (u < r) acc[u] = fma(w[x], ts[u * l + j0 + x], acc[u]);
+      for (int y = 0; y < PF; ++y) {
+        const int64_t i = i0 + 128 * x;
+        w[x][y] = (j0 + y < l && i < op.m) ? op.at(i, J[j0 + y]) : 0.0;
+      }
+#pragma unroll
+    for (int y = 0; y < PF; ++y) {
+      if (j0 + y < l) {
+        const double2 *c2 = reinterpret_cast<const double2 *>(ts + (j0 + y) * RMAX);
+#pragma unroll
+        for (int u2 = 0; u2 < RMAX / 2; ++u2) {
+          const double2 c = c2[u2];
+#pragma unroll
+          for (int x = 0; x < RR; ++x) {
+            acc[x][2 * u2] = fma(w[x][y], c.x, acc[x][2 * u2]);
+            acc[x][2 * u2 + 1] = fma(w[x][y], c.y, acc[x][2 * u2 + 1]);
+          }
+        }
       }
     }
   }
   double *A = a.A + b * a.a_stride;
 #pragma unroll
-  for (int u = 0; u < RMAX; ++u)
-    if (u < r) A[(int64_t)u * op.m + i] = acc[u];
+  for (int x = 0; x < RR; ++x) {
+    const int64_t i = i0 + 128 * x;
+    if (i < op.m)
+#pragma unroll
+      for (int u = 0; u < RMAX; ++u)
+        if (u < r) A[(int64_t)u * op.m + i] = acc[x][u];
+  }
 }
 
-// B = Sr^T * W[I,:]: one thread per column of B (all r outputs, ascending s), the k row
-// entries W[I[s], j] loaded 16 at a time.  grid (ceil(n/128), nb), 128 threads.
-template <int RMAX>
+// B = Sr^T * W[I,:]: thread = RR columns of B (all r outputs, ascending s).
+template <int RMAX, int RR>
 __global__ void __launch_bounds__(128) k_factor_B(FacArgs a) {
-  extern __shared__ double sr[];          // k x r: sr[t * k + s]
+  extern __shared__ __align__(16) double sr[];   // k x RMAX: sr[s * RMAX + u]
   const int64_t b = blockIdx.y;
   if (a.status[b] != LRA_OK) return;
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int k = a.k, r = a.r;
   const double *Sr = a.Sr + b * (int64_t)k * r;
-  for (int e = threadIdx.x; e < k * r; e += 128) sr[e] = Sr[e];
+  for (int e = threadIdx.x; e < k * RMAX; e += 128) {
+    const int s = e / RMAX, u = e % RMAX;
+    sr[e] = u < r ? Sr[u * k + s] : 0.0;
+  }
   __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  if (j >= op.n) return;
+  const int64_t j0c = (int64_t)blockIdx.x * (128 * RR) + threadIdx.x;
+  if (j0c >= op.n) return;
   const int64_t *I = a.I + b * k;
-  double acc[RMAX];
+  double acc[RR][RMAX];
 #pragma unroll
-  for (int u = 0; u < RMAX; ++u) acc[u] = 0.0;
-  for (int s0 = 0; s0 < k; s0 += 16) {
-    double w[16];
+  for (int x = 0; x < RR; ++x)
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      const int s = s0 + x;
-      w[x] = s < k ? (a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j)) : 0.0;
-    }
+    for (int u = 0; u < RMAX; ++u) acc[x][u] = 0.0;
+  constexpr int PF = 8;
+  for (int s0 = 0; s0 < k; s0 += PF) {
+    double w[RR][PF];
 #pragma unroll
-    for (int x = 0; x < 16; ++x) {
-      if (s0 + x < k) {
+    for (int x = 0; x < RR; ++x)
 #pragma unroll
-        for (int u = 0; u < RMAX; ++u)
-          if (u < r) acc[u] = fma(sr[u * k + s0 + x], w[x], acc[u]);
+      for (int y = 0; y < PF; ++y) {
+        const int s = s0 + y;
+        const int64_t j = j0c + 128 * x;
+        w[x][y] = (s < k && j < op.n) ? (a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j)) : 0.0;
+      }
+#pragma unroll
+    for (int y = 0; y < PF; ++y) {
+      if (s0 + y < k) {
+        const double2 *c2 = reinterpret_cast<const double2 *>(sr + (s0 + y) * RMAX);
+#pragma unroll
+        for (int u2 = 0; u2 < RMAX / 2; ++u2) {
+          const double2 c = c2[u2];
+#pragma unroll
+          for (int x = 0; x < RR; ++x) {
+            acc[x][2 * u2] = fma(c.x, w[x][y], acc[x][2 * u2]);
+            acc[x][2 * u2 + 1] = fma(c.y, w[x][y], acc[x][2 * u2 + 1]);
+          }
+        }
       }
     }
   }
   double *B = a.B + b * a.b_stride;
 #pragma unroll
-  for (int u = 0; u < RMAX; ++u)
-    if (u < r) B[j * r + u] = acc[u];
+  for (int x = 0; x < RR; ++x) {
+    const int64_t j = j0c + 128 * x;
+    if (j < op.n)
+#pragma unroll
+      for (int u = 0; u < RMAX; ++u)
+        if (u < r) B[j * r + u] = acc[x][u];
+  }
 }
 
 cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf) {
@@ -425,17 +472,21 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
     *nlaunch += 1;
     return cudaSuccess;
   }
-  dim3 gA((unsigned)((fa.op.m + 127) / 128), (unsigned)nb);
-  const size_t sA = (size_t)fa.l * fa.r * 8, sB = (size_t)fa.k * fa.r * 8;
-  void (*kA)(FacArgs) = fa.r <= 16 ? k_factor_A<16> : (fa.r <= 32 ? k_factor_A<32> : k_factor_A<64>);
-  void (*kB)(FacArgs) = fa.r <= 16 ? k_factor_B<16> : (fa.r <= 32 ? k_factor_B<32> : k_factor_B<64>);
+  static const int rr_env = getenv("LRA_FAC_RR") ? atoi(getenv("LRA_FAC_RR")) : 1;   // diagnostics
+  const int RM = fa.r <= 16 ? 16 : (fa.r <= 32 ? 32 : 64), RRf = (RM <= 32 && rr_env == 2) ? 2 : 1;
+  dim3 gA((unsigned)((fa.op.m + 128 * RRf - 1) / (128 * RRf)), (unsigned)nb);
+  const size_t sA = (size_t)fa.l * RM * 8, sB = (size_t)fa.k * RM * 8;
+  void (*kA)(FacArgs) = RM == 16 ? (RRf == 2 ? k_factor_A<16, 2> : k_factor_A<16, 1>)
+                        : (RM == 32 ? (RRf == 2 ? k_factor_A<32, 2> : k_factor_A<32, 1>) : k_factor_A<64, 1>);
+  void (*kB)(FacArgs) = RM == 16 ? (RRf == 2 ? k_factor_B<16, 2> : k_factor_B<16, 1>)
+                        : (RM == 32 ? (RRf == 2 ? k_factor_B<32, 2> : k_factor_B<32, 1>) : k_factor_B<64, 1>);
   if ((e = cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sA)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sB)) != cudaSuccess) return e;
   pf->begin("k_factor_A", st);
   kA<<<gA, 128, sA, st>>>(fa);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  dim3 gB((unsigned)((fa.op.n + 127) / 128), (unsigned)nb);
+  dim3 gB((unsigned)((fa.op.n + 128 * RRf - 1) / (128 * RRf)), (unsigned)nb);
   pf->begin("k_factor_B", st);
   kB<<<gB, 128, sB, st>>>(fa);
   pf->end(st);

@@ -25,6 +25,7 @@ mats = {"cfg2": synth.config2(0), "cfg1": synth.config1(0),
 cases = [("cfg2", 48, 48, 32), ("cfg2", 96, 96, 64), ("cfg2", 112, 112, 100), ("cfg2", 64, 128, 50), ("cfg2", 33, 33, 20),
          ("cfg2", 8, 13, 7), ("cfg2", 13, 8, 7), ("cfg2", 32, 48, 32), ("cfg1", 8, 8, 8), ("cauchy", 20, 20, 16)]
 times = {}
+ftimes = {}
 for name, k, l, r in cases:
     W = mats[name]
     m, n = W.shape
@@ -41,6 +42,7 @@ for name, k, l, r in cases:
         torch.cuda.synchronize()
         prof = h.profile_read()
         times[f"{name}_{k}x{l}"] = round(prof["k_nucleus"][0] * 1e3, 1)
+        ftimes[f"{name}_{k}x{l}"] = (round(prof["k_factor_A"][0] * 1e3, 1), round(prof["k_factor_B"][0] * 1e3, 1))
         key = f"{name}_{k}_{l}_{r}_{rep}"
         out[key + "_U"] = U.cpu().numpy()
         out[key + "_A"] = A.cpu().numpy()
@@ -48,3 +50,4 @@ for name, k, l, r in cases:
         out[key + "_st"] = st.cpu().numpy()
 np.savez(sys.argv[1], **out)
 print({"nucleus_us": times})
+print({"factors_us": ftimes})
