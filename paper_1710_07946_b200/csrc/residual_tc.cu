@@ -555,8 +555,11 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
         slot_ld = (slot_ld + 1) % WR;
       }
       double num = 0.0, den = 0.0;
+      int sb_next = first < c1 ? __ldg(sbcol + first * BN) : 0;   // column scale, one tile ahead
       for (int64_t ct = first; ct < c1; ct += 2) {
         const int64_t kk = k + (ct - c0);               // global tile counter (parity == grp)
+        const int sb_cur = sb_next;
+        if (ct + 2 < c1) sb_next = __ldg(sbcol + (ct + 2) * BN);
         {
           const int64_t cn = ct + 2 * (WR - 1);
           if (cn < c1) load_w(cn, slot_ld);
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(NTC, 1) k_residual_tc(TcArgs a) {
           slot_ld = (slot_ld + 1) % WR;
         }
         const int tb = (int)(kk & 1);
-        const int ex = eai + __ldg(sbcol + ct * BN);    // scale of this tile
+        const int ex = eai + sb_cur;                    // scale of this tile
         const double sc = ex > 0 ? __hiloint2double(ex << 20, 0) : 0.0;
         long long te0 = RTC_CLK();
         mbar_wait(B_TFULL + 8 * tb, (uint32_t)((kk >> 1) & 1));
