@@ -916,3 +916,29 @@ def test_new_entry_points_reject_bad_arguments(P, h):
     with pytest.raises(L.LraError) as e:
         L.lra_preprocess(h, Wd, L.Multiplier(M), torch.empty((8, 256), dtype=torch.float64, device="cuda"))
     assert e.value.status == L.LRA_EINVAL
+
+
+def test_config2_batch_in_bench_configuration(P, h):
+    """The bench's own launch configuration: lra_batch over 42 config-2 matrices (seeds as in
+    bench.py, ARHT d = 4, r = 32, k = l = 48, 3 sweeps, PRECISE residual, batch groups on the
+    side streams): every block reports OK with dominance certificates <= 1 + 1e-12, and three
+    sampled blocks (first, middle, last) equal the oracle (pivots bit-exact, rho 1e-4)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1710_07946_b200 import pipeline
+    nb = 42
+    seeds = [80000 + i for i in range(nb)]
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        Ws = list(ex.map(lambda s: synth.config2(s), seeds))
+    Wt = torch.from_numpy(np.ascontiguousarray(np.stack([W.T for W in Ws]))).cuda()
+    Md = synth.multiplier_abridged(0, 4096, 4, 48, "arht")
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), P.lra.Multiplier(Md), 32, 48, 3, nb)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)
+    assert np.all(st["status"] == 0)
+    assert np.all(st["cert_rows"] <= 1 + 1e-12) and np.all(st["cert_cols"] <= 1 + 1e-12)
+    for b in (0, nb // 2, nb - 1):
+        ora = O.cur_pipeline(Ws[b], Md, 32, 48, 48, 3)
+        assert list(bufs.I[b].cpu().numpy()) == list(ora.I)
+        assert list(bufs.J[b].cpu().numpy()) == list(ora.J)
+        rho = float(np.sqrt(bufs.num2[b].item() / bufs.den2[b].item()))
+        assert abs(rho / ora.rho - 1) <= 1e-4, (b, rho, ora.rho)
