@@ -2,20 +2,35 @@
 """bench.py — throughput of the superfast-CUR hot path on B200 (BASELINE.json metric:
 "CUR LRA matrices/sec and preprocess+residual GB/s vs HBM peak, 1/2/4/8 B200").
 
-One step = one pass of the whole hot path (§8(a): sketch, C-A sweeps, nucleus + factors,
-full a-posteriori check) over one batch of B synthetic config-2 matrices per GPU
-(W = U·diag(σ)·Vᵀ fp32 4096², r = 32, k = l = 48, ARHT d = 4, 3 sweeps), through
-``lra_batch``.  Two batches alternate, so consecutive steps never find their inputs in L2
-(2·B·67 MB > 126 MB).  N > 1: one process per GPU (torchrun), independent matrices per
-rank, no collective on the data path ("weak" scaling), max-over-ranks device time.
+Headline (default, ``--workload cfg2``): one step = the whole hot path (§8(a): sketch, C-A
+sweeps, nucleus + factors, full a-posteriori check) over one batch of B synthetic config-2
+matrices per GPU (W = U·diag(σ)·Vᵀ fp32 4096², r = 32, k = l = 48, ARHT d = 4, 3 sweeps)
+through ``lra_batch``.  Two batches alternate, so consecutive steps never find their inputs in
+L2 (2·B·67 MB > 126 MB).  N > 1: one process per GPU, independent matrices per rank, no
+collective on the data path ("weak"), max-over-ranks device time.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl native|reference]
+Measurement protocol (VERDICT r1 "make the measurement honest"):
+  * the headline region runs with kernel profiling OFF (the overlapped schedule as shipped);
+  * an ISOLATION pass then replays the same batches with profiling on: lra_batch runs its
+    groups in order on one stream and every kernel is bracketed by events on its launch
+    stream, so each kernel's interval is its own device time (Σ kernel ms ≤ the isolated
+    step); ``roofline`` and ``stage_rooflines`` are computed from those device times;
+  * secondary workloads in the same line (``workloads``): config 5 (131072² fp32 = 68.7 GB,
+    row-sharded over the N ranks, each rank generating its shard on device) with the
+    preprocess and residual GB/s the metric names, and config 3 (4096 Cauchy blocks dealt
+    out across ranks) in blocks/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--workload cfg2|cfg5|cfg3]
+                  [--impl native|reference] [--no-extra] [--no-e2e] [--no-cpu-baseline]
+  N > 1 without WORLD_SIZE in the environment: bench.py starts N ranks itself through
+  torch.distributed.run (127.0.0.1).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -27,11 +42,23 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# ---------------------------------------------------------------- workload definitions
 M_ROWS = N_COLS = 4096
 R, K, SWEEPS, DEPTH = 32, 48, 3, 4
 WORKLOAD = (f"cfg2-arht: W=U*diag(s)*V^T fp32 {M_ROWS}x{N_COLS}, s_i=1 (i<=32) then 1e-6*0.9^(i-32); "
-            f"r={R}, k=l={K}, ARHT d={DEPTH} +-1 diagonal, {SWEEPS} C-A sweeps, full residual")
+            f"r={R}, k=l={K}, ARHT d={DEPTH} +-1 diagonal, {SWEEPS} C-A sweeps, full residual (PRECISE)")
 METRIC = "CUR LRA matrices/sec (config 2, ARHT) — sketch+C-A+nucleus+residual"
+
+C5_M = C5_N = 131072
+C5_R, C5_K, C5_D, C5_T = 64, 96, 5, 3
+C5_WORKLOAD = (f"cfg5: W=U*diag(s)*V^T+N fp32 {C5_M}x{C5_N} (68.7 GB) row-sharded, s_i=10^(-3(i-1)/63), "
+               f"N~N(0,1e-8); r={C5_R}, k=l={C5_K}, ARHT d={C5_D}, {C5_T} sweeps, full residual (FAST)")
+C5_METRIC = "CUR LRA matrices/sec (config 5, 131072^2 row-sharded) — sketch+C-A+nucleus+residual"
+
+C3_NB, C3_M, C3_R, C3_K, C3_T = 4096, 512, 16, 20, 2
+C3_WORKLOAD = (f"cfg3: {C3_NB} Cauchy blocks W_ij=fl32(1/(s_i-t_j)) {C3_M}x{C3_M}, s~U[0,1], t~U[2,3]; "
+               f"sparse +-1 (4/col), r={C3_R}, k=l={C3_K}, {C3_T} sweeps, full residual (PRECISE); blocks dealt to ranks")
+C3_METRIC = "CUR LRA blocks/sec (config 3, FMM Cauchy blocks) — sketch+C-A+nucleus+residual"
 
 
 def _peaks():
@@ -50,19 +77,24 @@ def _dist():
     return ws, rank, lrank
 
 
-def _gen_batch(seeds):
-    import synth
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        Ws = list(ex.map(lambda s: synth.config2(s, n=N_COLS), seeds))
-    out = np.empty((len(seeds), N_COLS, M_ROWS), dtype=np.float32)
-    for i, W in enumerate(Ws):
-        out[i] = W.T
-    return out
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _spawn(args_in):
+    """--gpus N > 1 outside torchrun: start N ranks (one process per GPU) and wait."""
+    n = args_in.gpus
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class Clocks:
-    """nvidia-smi sampler (200 ms) for the clocks line of the JSON."""
+    """nvidia-smi sampler (50 ms) for the clocks line of the JSON."""
 
     def __init__(self, dev):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -107,8 +139,6 @@ class Clocks:
         os.unlink(self.f.name)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        # samples while the GPU was busy: keep the top half by clock (idle samples sit at max
-        # too, but the warm-up + timed region dominate the sampler's lifetime)
         sm = [r[0] for r in rows]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower().startswith("active")})
@@ -126,16 +156,36 @@ def _oracle_cores():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(n_mats=4):
-    """The oracle as it stands on the host cores, on a bounded sample of the same workload."""
+# ---------------------------------------------------------------- reference arm (the oracle)
+def _oracle_cfg2(n_mats, seed0):
     import synth
     from oracle import lra as O
     mult = synth.multiplier_abridged(0, N_COLS, DEPTH, K, "arht")
-    Ws = [synth.config2(90000 + i, n=N_COLS) for i in range(n_mats)]
+    Ws = [synth.config2(seed0 + i, n=N_COLS) for i in range(n_mats)]
     t = time.perf_counter()
     for W in Ws:
         O.cur_pipeline(W, mult, R, K, K, SWEEPS)
-    dt = time.perf_counter() - t
+    return time.perf_counter() - t
+
+
+def _oracle_cfg3(n_blocks, seed):
+    import synth
+    from oracle import lra as O
+    s, t = synth.cauchy_params(seed, n_blocks, C3_M, C3_M)
+    mult = synth.multiplier_sparse_batch(seed, n_blocks, C3_M, C3_K)
+    per = C3_K * 4
+    Ws = [synth.cauchy_block(s[b], t[b]) for b in range(n_blocks)]
+    t0 = time.perf_counter()
+    for b in range(n_blocks):
+        mb = {"kind": "sparse", "lbar": C3_K, "nnz": 4, "sp_row": mult["sp_row"][b * per:(b + 1) * per],
+              "sp_sign": mult["sp_sign"][b * per:(b + 1) * per]}
+        O.cur_pipeline(Ws[b], mb, C3_R, C3_K, C3_K, C3_T)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(n_mats=4):
+    """The oracle as it stands on the host cores, on a bounded sample of the same workload."""
+    dt = _oracle_cfg2(n_mats, 90000)
     return {"value": n_mats / dt, "unit": "matrices/s", "cores": _oracle_cores(), "kind": "oracle",
             "sample": f"{n_mats} config-2 matrices (full size) through oracle.cur_pipeline, {dt:.1f} s"}
 
@@ -144,85 +194,273 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    import synth
-    from oracle import lra as O
-    mult = synth.multiplier_abridged(0, N_COLS, DEPTH, K, "arht")
-    Ws = [synth.config2(80000 + i, n=N_COLS) for i in range(args.warmup + args.steps)]
-    for W in Ws[:args.warmup]:
-        O.cur_pipeline(W, mult, R, K, K, SWEEPS)
-    t = time.perf_counter()
-    for W in Ws[args.warmup:]:
-        O.cur_pipeline(W, mult, R, K, K, SWEEPS)
-    dt = time.perf_counter() - t
-    v = args.steps / dt
     cores = _oracle_cores()
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "matrices/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+    if args.workload == "cfg5":
+        print(json.dumps({"impl": "reference", "unavailable": "the fp64 oracle needs the 68.7 GB config-5 matrix in "
+                          "host RAM and hours per step; the reference arm runs cfg2 / cfg3"}), flush=True)
+        return
+    if args.workload == "cfg3":
+        nb = 8
+        for _ in range(args.warmup):
+            _oracle_cfg3(1, 7)
+        dts = [_oracle_cfg3(nb, 100 + i) for i in range(args.steps)]
+        v = nb * args.steps / sum(dts)
+        metric, unit, wl, sample = C3_METRIC, "blocks/s", C3_WORKLOAD, f"{nb} config-3 blocks per step"
+    else:
+        for i in range(args.warmup):
+            _oracle_cfg2(1, 70000 + i)
+        dts = [_oracle_cfg2(1, 80000 + i) for i in range(args.steps)]
+        v = args.steps / sum(dts)
+        metric, unit, wl, sample = METRIC, "matrices/s", WORKLOAD, "1 full-size config-2 matrix per step"
+    line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(dts) / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "batch_per_step": 1,
+            "data": "synthetic", "config": {"workload": wl,
                                            "note": "reference arm = the fp64 numpy oracle (no reference code exists)"},
-            "cpu_baseline": {"value": v, "unit": "matrices/s", "cores": cores, "kind": "oracle",
-                             "sample": f"1 full-size config-2 matrix per step, {args.steps} steps"},
-            "e2e": {"value": v, "unit": "matrices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle",
+                             "sample": f"{sample}, {args.steps} steps"},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def algorithmic(name, mult, B):
-    """Algorithmic bytes (and flops) of one launch of `name` over a batch of B matrices
-    (DESIGN.md §6): what the method must move, not what the kernel happens to move."""
+# ---------------------------------------------------------------- algorithmic bytes
+def _fibers(mult, n, d):
+    s = n >> d
+    return len({int(c) % s for c in mult["col"]})
+
+
+def alg_bytes_cfg2(name, mult, mats, loops=SWEEPS):
+    """Algorithmic bytes of `name` over `mats` config-2 matrices (what the method must move)."""
     m, n = M_ROWS, N_COLS
-    s = n >> DEPTH
-    fibers = len({int(c) % s for c in mult["col"]})
     if name.startswith("k_sketch"):
-        return B * (m * (1 << DEPTH) * fibers * 4 + m * K * 8), 0.0
-    if name == "k_residual":
-        return B * (m * n * 4 + (m * R + R * n) * 8), B * 2.0 * m * n * R
-    if name == "k_residual_tc":   # W once + the int8 digit slices of A and B (6 each)
-        return B * (m * n * 4 + (m + n) * R * 6), B * 2.0 * m * n * R * 21
-    if name == "k_ca":
-        return B * SWEEPS * (m * K + K * n) * 4, 0.0
-    return 0, 0.0
+        return mats * (m * (1 << DEPTH) * _fibers(mult, n, DEPTH) * 4 + m * K * 8)
+    if name == "k_residual_tc":
+        return mats * m * n * 4
+    if name == "residual_stage":      # split + tensor-core pass + reduce: W once, A and B once
+        return mats * (m * n * 4 + (m * R + R * n) * 8)
+    if name == "k_ca":                # Y block + per loop W[I,:] and W[:,J] (SURVEY §8(d) gathers)
+        return mats * (m * K * 8 + loops * (K * n + m * K) * 4)
+    return 0
 
 
-def ncu_traffic(kname, mats_per_launch):
-    """dram read+write bytes per launch of kname from the committed ncu --set full summary
-    (profiles/<round>/ncu_full_final.txt), scaled from that capture's problems per launch."""
+def _roof(name, byts, ms_per_launch, peaks, src):
+    ach = byts / (ms_per_launch * 1e-3) / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / peaks["hbm_gbs"], "peak_source": src, "traffic": None,
+            "ms_per_launch": ms_per_launch}
+
+
+def _ncu_traffic(kname, mats_per_launch):
+    """dram read+write bytes per launch of kname from the newest committed ncu --set full summary
+    (profiles/<round>/ncu_full*.txt), scaled to mats_per_launch."""
     import glob
     import re
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*",
-                                          "ncu_full_final.txt")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_final.txt")))
     key = {"k_ca": "k_cacl"}.get(kname, kname)
+
+    def val(x):
+        x = x.strip()
+        f = float(x.split()[0])
+        return f * (1e9 if "Gbyte" in x else 1e6 if "Mbyte" in x else 1e3 if "Kbyte" in x else 1)
+
     for path in reversed(files):
         for line in open(path):
             if not line.startswith("Kernel Name=") or key not in line.split(";")[0]:
                 continue
             f = dict(kv.split("=", 1) for kv in (x.strip() for x in line.split(";")) if "=" in kv)
-            rd = float(f["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in f["dram__bytes_read.sum"] else 1e9 if "Gbyte" in f["dram__bytes_read.sum"] else 1e3)
-            wr = float(f["dram__bytes_write.sum"].split()[0]) * (1e6 if "Mbyte" in f["dram__bytes_write.sum"] else 1e9 if "Gbyte" in f["dram__bytes_write.sum"] else 1e3)
-            grid = int(re.sub(r"[^0-9]", "", f.get("launch__grid_size", "0")) or 0)
-            cdim = int(re.sub(r"[^0-9]", "", f.get("launch__cluster_dim_x", "0")) or 0)
-            if key == "k_cacl" and grid and cdim:
-                cap_mats = grid / cdim
-            elif key.startswith("k_residual"):
-                cap_mats = rd / (4096 * 4096 * 4)
-            else:
-                return None
-            return {"bytes_per_launch": (rd + wr) / cap_mats * mats_per_launch,
-                    "source": os.path.relpath(path, os.path.dirname(os.path.abspath(__file__)))}
+            rd, wr = val(f["dram__bytes_read.sum"]), val(f["dram__bytes_write.sum"])
+            mats = f.get("matrices_per_launch")
+            if mats is None:
+                grid = int(re.sub(r"[^0-9]", "", f.get("launch__grid_size", "0")) or 0)
+                cdim = int(re.sub(r"[^0-9]", "", f.get("launch__cluster_dim_x", "0")) or 0)
+                if key == "k_cacl" and grid and cdim:
+                    mats = grid / cdim
+                elif key.startswith("k_residual"):
+                    mats = rd / (M_ROWS * N_COLS * 4)
+                else:
+                    return None
+            return {"bytes_per_launch": (rd + wr) / float(mats) * mats_per_launch,
+                    "source": os.path.relpath(path, ROOT)}
     return None
 
 
+def _gen_batch(seeds):
+    import synth
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        Ws = list(ex.map(lambda s: synth.config2(s, n=N_COLS), seeds))
+    out = np.empty((len(seeds), N_COLS, M_ROWS), dtype=np.float32)
+    for i, W in enumerate(Ws):
+        out[i] = W.T
+    return out
+
+
+def _max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _timed(fn, steps, ws, st):
+    """steps calls of fn bracketed by a barrier + synchronize, CUDA events on stream st; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(steps):
+        fn(i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    return _max_over_ranks(e0.elapsed_time(e1), ws)
+
+
+def _isolated(h, fn, steps, ws):
+    """Isolation pass: profiling on (lra_batch groups serialized on one stream, an event pair
+    per kernel on its launch stream).  Returns ({kernel: (ms per step, launches per step)},
+    isolated ms per step)."""
+    import torch
+    torch.cuda.synchronize()
+    h.profile(True)
+    t = _timed(fn, steps, 1, torch.cuda.current_stream())
+    prof = h.profile_read()
+    h.profile(False)
+    return {k: (v[0] / steps, v[1] / steps) for k, v in prof.items()}, t / steps
+
+
+# ---------------------------------------------------------------- secondary workloads
+def run_cfg5(h, ws, rank, lrank, steps, warmup, peaks, src):
+    """Config 5 at full size, row-sharded over the ws ranks (each generates its shard on device)."""
+    import torch
+    import synth
+    from paper_1710_07946_b200 import lra
+    m, n = C5_M, C5_N
+    rows = m // ws
+    row0 = rank * rows
+    t0 = time.time()
+    U, V = synth.config5_factors(0, m, n)
+    Wt = synth.config5_torch(0, m, n, row0=row0, rows=rows, factors=(U, V))
+    del U, V
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    mult = synth.multiplier_abridged(0, n, C5_D, C5_K, "arht")
+    M = lra.Multiplier(mult)
+    W = lra.Dense(Wt, row0=row0, m_global=m if ws > 1 else 0)      # one rank: the unsharded path
+    f64 = dict(dtype=torch.float64, device="cuda")
+    Y = torch.empty((C5_K, rows), **f64)
+    I = torch.empty(C5_K, dtype=torch.int64, device="cuda")
+    J = torch.empty(C5_K, dtype=torch.int64, device="cuda")
+    Uo = torch.empty((C5_K, C5_K), **f64)
+    A = torch.empty((C5_R, rows), **f64)
+    B = torch.empty((n, C5_R), **f64)
+    num2 = torch.empty(1, **f64)
+    den2 = torch.empty(1, **f64)
+    stats = lra.new_stats(1, "cuda")
+
+    def step(i):
+        lra.lra_preprocess(h, W, M, Y)
+        lra.lra_cross_approx(h, W, Y, None, C5_R, C5_K, C5_K, C5_T, I, J, Uo, A, B, stats)
+        lra.lra_cur_residual(h, W, A, B, C5_R, num2, den2, prec=lra.LRA_RECON_FAST)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    l0 = h.launches()
+    ms = _timed(step, steps, ws, torch.cuda.current_stream()) / steps
+    launches = (h.launches() - l0) / steps
+    prof, iso_ms = _isolated(h, step, 1, ws)
+    st = lra.stats_to_numpy(stats)[0]
+    rho = float(np.sqrt(num2.item() / den2.item()))
+    sk = sum(v[0] for k, v in prof.items() if k.startswith("k_sketch"))
+    rs = sum(v[0] for k, v in prof.items() if k in ("k_split", "k_residual_tc", "k_reduce"))
+    rtc = prof.get("k_residual_tc", (0.0, 1))[0]
+    sk, rs, rtc = (_max_over_ranks(x, ws) for x in (sk, rs, rtc))
+    sk_bytes = m * (1 << C5_D) * _fibers(mult, n, C5_D) * 4 + m * C5_K * 8
+    rs_bytes = m * n * 4 + (m * C5_R + C5_R * n) * 8
+    out = {"metric": C5_METRIC, "value": 1e3 / ms, "unit": "matrices/s", "ms_per_step": ms, "steps": steps,
+           "scaling": "strong", "config": {"workload": C5_WORKLOAD, "rows_per_rank": rows, "gen_s": round(gen_s, 1),
+                                           "l2": "inputs_gt_l2 (8.6-68.7 GB per rank)"},
+           "isolated_ms_per_step": iso_ms, "kernels_ms": {k: v[0] for k, v in prof.items()},
+           "preprocess": _roof("k_sketch (aggregate)", sk_bytes, sk, peaks, src) if sk > 0 else None,
+           "residual": _roof("split+k_residual_tc+reduce (aggregate)", rs_bytes, rs, peaks, src) if rs > 0 else None,
+           "residual_tc_only": _roof("k_residual_tc (aggregate, W bytes)", m * n * 4, rtc, peaks, src) if rtc > 0 else None,
+           "gpu_launches_per_step": launches,
+           "status": int(st["status"]), "rho": rho, "lu_steps": int(st["lu_steps"]), "swaps": int(st["swaps"]),
+           "cert_rows": float(st["cert_rows"]), "cert_cols": float(st["cert_cols"])}
+    for key in ("preprocess", "residual", "residual_tc_only"):
+        if out[key] and ws > 1:
+            out[key]["per_gpu_frac"] = out[key]["frac"] / ws
+    del Wt
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_cfg3(h, ws, rank, steps, warmup, peaks, src):
+    """Config 3: the 4096 Cauchy blocks dealt out in contiguous ranges, lra_batch per rank."""
+    import torch
+    import synth
+    from paper_1710_07946_b200 import lra, pipeline
+    per = C3_NB // ws
+    b0 = rank * per
+    s, t = synth.cauchy_params(0, C3_NB, C3_M, C3_M)
+    Wt = synth.cauchy_blocks_torch(s[b0:b0 + per], t[b0:b0 + per], "cuda")
+    mult = synth.multiplier_sparse_batch(0, C3_NB, C3_M, C3_K)
+    nnz = C3_K * 4
+    mb = dict(mult)
+    mb["sp_row"] = mult["sp_row"][b0 * nnz:(b0 + per) * nnz]
+    mb["sp_sign"] = mult["sp_sign"][b0 * nnz:(b0 + per) * nnz]
+    M = lra.Multiplier(mb)
+    W = lra.Dense(Wt)
+    bufs = pipeline.BatchBuffers(per, C3_R, C3_K)
+
+    def step(i):
+        pipeline.cur_batch(h, W, M, C3_R, C3_K, C3_T, per, bufs=bufs)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    ms = _timed(step, steps, ws, torch.cuda.current_stream()) / steps
+    prof, iso_ms = _isolated(h, step, 1, ws)
+    st = lra.stats_to_numpy(bufs.stats)
+    rho = np.sqrt(bufs.num2.cpu().numpy() / bufs.den2.cpu().numpy())
+    w_bytes = C3_NB * C3_M * C3_M * 4
+    out = {"metric": C3_METRIC, "value": C3_NB / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
+           "steps": steps, "scaling": "strong (fixed 4096-block batch dealt to ranks)",
+           "config": {"workload": C3_WORKLOAD, "blocks_per_rank": per},
+           "hbm_frac_of_step": (w_bytes / ws) / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+           "isolated_ms_per_step": iso_ms, "kernels_ms": {k: v[0] for k, v in prof.items()},
+           "ok_blocks": int(np.sum(st["status"] == 0)), "median_rho": float(np.median(rho))}
+    del Wt
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------- headline (config 2)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=42)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "cfg3"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary workloads (cfg5, cfg3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/baseline (for ncu)")
+    ap.add_argument("--profile-only", action="store_true", help="few steps, no clocks/e2e/baseline/extras (for ncu)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     if args.warmup < 3 and not args.profile_only:
         args.warmup = 3
     if args.impl == "reference":
@@ -232,21 +470,47 @@ def main():
     import torch.distributed as dist
 
     import synth
-    from paper_1710_07946_b200 import Handle, lra, pipeline
+    from paper_1710_07946_b200 import Handle, lra, nccl_unique_id, pipeline
 
     ws, rank, lrank = _dist()
+    if ws != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; measuring {ws} rank(s)", file=sys.stderr)
     torch.cuda.set_device(lrank)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    peaks, peaks_src = _peaks()
+    # the handle: an NCCL communicator over the ranks for the row-sharded config-5 path
+    nid = [None]
+    if ws > 1:
+        nid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+    h = Handle(lrank, nccl_id=nid[0], nranks=ws, rank=rank)
+    st = torch.cuda.current_stream()
+
+    if args.workload != "cfg2":
+        fn = run_cfg5 if args.workload == "cfg5" else run_cfg3
+        a = (h, ws, rank, lrank) if args.workload == "cfg5" else (h, ws, rank)
+        clocks = None if args.profile_only else Clocks(lrank)
+        t0 = time.time()
+        res = fn(*a, max(1, args.steps), args.warmup, peaks, peaks_src)
+        if clocks:
+            clocks.window(t0, time.time())
+        if rank == 0:
+            res.update({"n_gpus": ws, "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None,
+                        "dtype": "f64", "data": "synthetic", "clocks": clocks.stop() if clocks else None,
+                        "gpu": torch.cuda.get_device_name(lrank)})
+            print(json.dumps(res), flush=True)
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
     B = args.batch
     mult = synth.multiplier_abridged(0, N_COLS, DEPTH, K, "arht")
     M = lra.Multiplier(mult)
     host = [_gen_batch([rank * 100000 + p * B + i for i in range(B)]) for p in range(2)]
-    pools = [torch.from_numpy(h).cuda() for h in host]
+    pools = [torch.from_numpy(hb).cuda() for hb in host]
     Ws = [lra.Dense(p) for p in pools]
-    h = Handle(lrank)
     bufs = pipeline.BatchBuffers(B, R, K)
-    st = torch.cuda.current_stream()
 
     def step(i):
         pipeline.cur_batch(h, Ws[i % 2], M, R, K, SWEEPS, B, bufs=bufs)
@@ -257,121 +521,140 @@ def main():
     stats = lra.stats_to_numpy(bufs.stats)
     assert np.all(stats["status"] == 0), stats
     clocks = None if args.profile_only else Clocks(lrank)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    h.profile(True)
     l0 = h.launches()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     t0 = time.time()
-    e0.record(st)
-    for i in range(args.steps):
-        step(i)
-    e1.record(st)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
+    ms = _timed(step, args.steps, ws, st)
     t1 = time.time()
     if clocks:
         clocks.window(t0, t1)
-    ms = e0.elapsed_time(e1)
     launches = h.launches() - l0
-    prof = h.profile_read()
-    h.profile(False)
-    if ws > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
     clk = clocks.stop() if clocks else None
     total = ws * B * args.steps
     value = total / (ms / 1e3)
-    peaks, peaks_src = _peaks()
+    stats = lra.stats_to_numpy(bufs.stats)
+    mean_loops = float(np.mean(stats["loops_done"]))
+    pivot_steps = float(np.mean(stats["lu_steps"] + stats["swaps"]))
 
-    # ---- roofline of the dominant kernel (live CUDA-event timing inside the timed region)
-    dom = max(prof.items(), key=lambda kv: kv[1][0])
-    name, (kms, cnt) = dom
-    per_launch_s = kms / cnt / 1e3
-    # one launch processes one batch group: B * steps / (launches of this kernel in the region)
-    per_launch_mats = B * args.steps / cnt
-    byts, flops = algorithmic(name, mult, per_launch_mats)
-    if name == "k_ca":
-        ach = byts / per_launch_s / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src, "traffic": None,
-                "note": "latency-bound pivot chain (DESIGN.md §6.1): the algorithmic gather bytes over the launch "
-                        "time; see 'latency' for the per-step cost",
-                "latency": {"launch_ms": kms / cnt, "matrices_per_launch": per_launch_mats,
-                            "pivot_steps_per_matrix": float(np.mean(stats["lu_steps"] + stats["swaps"])),
-                            "us_per_pivot_step": kms / cnt * 1e3 / max(1.0, float(np.mean(stats["lu_steps"] + stats["swaps"])))}}
-    elif name == "k_residual":
-        fp64_peak = float(os.environ.get("LRA_FP64_TFLOPS", "37.2"))
-        roof = {"kernel": name, "bound": "alu", "achieved": flops / per_launch_s / 1e12, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": flops / per_launch_s / 1e12 / fp64_peak,
-                "peak_source": "FP64 DFMA: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)",
-                "hbm_gbs": byts / per_launch_s / 1e9, "hbm_frac": byts / per_launch_s / 1e9 / peaks["hbm_gbs"],
-                "traffic": None}
+    # ---- isolation pass: the same two batches, kernels serialized, device time per kernel
+    iso_steps = 2
+    prof, iso_ms = _isolated(h, step, iso_steps, ws)
+    kern_sum = sum(v[0] for v in prof.values())
+    kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / kern_sum}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
+
+    def per_launch(name):
+        ms_step, nl = prof[name]
+        return ms_step / nl, B / nl         # ms per launch, matrices per launch
+
+    stage = {}
+    for name in prof:
+        if name.startswith("k_sketch"):
+            ml, mats = per_launch(name)
+            stage["preprocess"] = _roof(name, alg_bytes_cfg2(name, mult, mats), ml, peaks, peaks_src)
+        if name == "k_residual_tc":
+            ml, mats = per_launch(name)
+            stage["residual_tc"] = _roof(name, alg_bytes_cfg2(name, mult, mats), ml, peaks, peaks_src)
+            tr = _ncu_traffic(name, mats)
+            if tr:
+                stage["residual_tc"]["traffic"] = tr["bytes_per_launch"]
+                stage["residual_tc"]["traffic_source"] = tr["source"]
+    rs_ms = sum(prof[k][0] for k in ("k_split", "k_residual_tc", "k_reduce") if k in prof)
+    if rs_ms > 0:
+        stage["residual_stage"] = _roof("k_split+k_residual_tc+k_reduce", alg_bytes_cfg2("residual_stage", mult, B),
+                                        rs_ms, peaks, peaks_src)
+    ml, mats = per_launch(dom)
+    if dom in ("k_ca",):
+        roof = _roof(dom, alg_bytes_cfg2(dom, mult, mats, loops=mean_loops), ml, peaks, peaks_src)
+        roof["note"] = ("latency-bound pivot chain (DESIGN.md §6.1): algorithmic gather bytes over the isolated "
+                        "launch time; 'latency' gives the per-pivot-step cost")
+        roof["latency"] = {"launch_ms": ml, "matrices_per_launch": mats, "pivot_steps_per_matrix": pivot_steps,
+                           "us_per_pivot_step": ml * 1e3 / max(1.0, pivot_steps)}
     else:
-        ach = byts / per_launch_s / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "peak_source": peaks_src, "traffic": None}
-    tr = ncu_traffic(name, per_launch_mats)
-    if tr:
+        roof = dict(stage.get("residual_tc" if dom == "k_residual_tc" else "preprocess")
+                    or _roof(dom, 0, ml, peaks, peaks_src))
+    tr = _ncu_traffic(dom, mats)
+    if tr and roof.get("traffic") is None:
         roof["traffic"] = tr["bytes_per_launch"]
         roof["traffic_source"] = tr["source"]
-    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1],
-                   "share": v[0] / sum(x[0] for x in prof.values())} for k, v in prof.items()}
-    stage_gbs = {}
-    for k in ("k_sketch_arht", "k_residual", "k_residual_tc"):
-        if k in prof:
-            b, _ = algorithmic(k, mult, B * args.steps / prof[k][1])
-            stage_gbs[k] = b / (prof[k][0] / prof[k][1] / 1e3) / 1e9
 
-    # ---- e2e through the public API with host buffers (H2D of W, D2H of results, timed)
+    # ---- e2e through the public API with host buffers: H2D of each batch overlapped with the
+    # previous batch's compute (copy stream + events), D2H of the per-matrix results
     e2e = None
     if not args.no_e2e and not args.profile_only:
         pin = [torch.from_numpy(hb).pin_memory() for hb in host]
-        dev = torch.empty_like(pools[0])
-        Wd = lra.Dense(dev)
-        outs = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2)]
-        ke = max(3, min(args.steps, 10))
-        for i in range(2):
-            dev.copy_(pin[i % 2], non_blocking=True)
-            pipeline.cur_batch(h, Wd, M, R, K, SWEEPS, B, bufs=bufs)
+        dev = [torch.empty_like(pools[0]) for _ in range(2)]
+        Wd = [lra.Dense(d) for d in dev]
+        outs = [[torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (bufs.I, bufs.J, bufs.U, bufs.num2,
+                                                                           bufs.den2)] for _ in range(2)]
+        cs = torch.cuda.Stream()
+        copied = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
+        ke = max(4, min(args.steps, 12))
+
+        def e2e_run(nsteps):
+            with torch.cuda.stream(cs):
+                dev[0].copy_(pin[0], non_blocking=True)
+                copied[0].record(cs)
+            for i in range(nsteps):
+                if i + 1 < nsteps:          # prefetch the next batch while this one computes
+                    with torch.cuda.stream(cs):
+                        if i >= 1:
+                            cs.wait_event(used[(i + 1) % 2])
+                        dev[(i + 1) % 2].copy_(pin[(i + 1) % 2], non_blocking=True)
+                        copied[(i + 1) % 2].record(cs)
+                st.wait_event(copied[i % 2])
+                pipeline.cur_batch(h, Wd[i % 2], M, R, K, SWEEPS, B, bufs=bufs)
+                used[i % 2].record(st)
+                for o, x in zip(outs[i % 2], (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2)):
+                    o.copy_(x, non_blocking=True)
+
+        e2e_run(2)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(st)
-        for i in range(ke):
-            dev.copy_(pin[i % 2], non_blocking=True)
-            pipeline.cur_batch(h, Wd, M, R, K, SWEEPS, B, bufs=bufs)
-            for o, x in zip(outs, (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2)):
-                o.copy_(x, non_blocking=True)
+        e2e_run(ke)
         f1.record(st)
         torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if ws > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+        ems = _max_over_ranks(f0.elapsed_time(f1), ws)
         d2h = sum(x.numel() * x.element_size() for x in (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2))
-        e2e = {"value": ws * B * ke / (ems / 1e3), "unit": "matrices/s",
-               "h2d_bytes_per_step": int(pools[0].numel() * 4), "d2h_bytes_per_step": int(d2h)}
+        h2d = int(pools[0].numel() * 4)
+        e2e = {"value": ws * B * ke / (ems / 1e3), "unit": "matrices/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(d2h), "h2d_GBs_per_gpu": h2d * ke / (ems / 1e3) / 1e9,
+               "note": "H2D of batch i+1 overlaps batch i's compute; PCIe-bound when h2d_GBs_per_gpu is near "
+                       "the host link rate"}
+        del dev, Wd, pin
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu = cpu_baseline()
+
+    # ---- secondary workloads (config 5 row-sharded, config 3 dealt), device-timed
+    extra = {}
+    if not args.no_extra and not args.profile_only:
+        del pools, Ws
+        torch.cuda.empty_cache()
+        for name, fn, a in (("cfg3", run_cfg3, (h, ws, rank)), ("cfg5", run_cfg5, (h, ws, rank, lrank))):
+            try:
+                extra[name] = fn(*a, 5 if name == "cfg5" else 10, 2 if name == "cfg5" else 3, peaks, peaks_src)
+            except Exception as ex:          # report, keep the headline
+                extra[name] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "batch_per_gpu": B, "l2": "inputs_gt_l2 (2 alternating batches of "
                            f"{B} x 67 MB per GPU)", "parallelism": f"dp{ws} (independent matrices per rank)"},
-                "roofline": roof, "stage_gbs": stage_gbs, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk,
-                "gpu": torch.cuda.get_device_name(lrank)}
+                "roofline": roof, "stage_rooflines": stage,
+                "isolation": {"ms_per_step": iso_ms, "kernel_ms_sum": kern_sum, "steps": iso_steps,
+                              "note": "same batches, lra_batch groups serialized on one stream, event pair per "
+                                      "kernel on its launch stream (device time, no queueing)"},
+                "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "workloads": extra, "gpu": torch.cuda.get_device_name(lrank)}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -173,7 +173,8 @@ lra_status lra_preprocess_full(lra_handle h, const lra_operand *W /* host struct
      A = W[:,J] T_r Sigma_r^{-1}  (m x r, ld m),   B = S_r^T W[I,:]  (r x n, ld r),
    so that CUR = A*B.  maxvol: pivot rule = smallest row-major index among |c| >= (1-tie_slack)*max
    (reading C11), stop when max |C'| <= 1 + swap_tol (C12), at most swap_cap swaps per call.
-   Requires 0 < r <= k == l (reading C9), k <= min(m, n), k <= 64.
+   Requires 0 < r <= k == l (reading C9), k <= min(m, n), k <= 112 (on-chip tiers for k <= 64,
+   the global-memory tier beyond and for blocks too tall for the on-chip tiers).
    y_complex != 0 means Y is complex128 (ARFT).  stats (device) may be NULL.
    Errors: EINVAL / EUNSUPPORTED synchronously; ESINGULAR in stats->status. */
 lra_status lra_cross_approx(lra_handle h, const lra_operand *W, const void *Y, int64_t ldy,
@@ -298,7 +299,9 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
                      lra_ca_stats *stats, void *stream);
 
 /* Kernel timing for measurement (bench.py): while enabled, every kernel this handle launches is
-   bracketed by a CUDA event pair recorded on its launch stream.  lra_profile_read synchronizes
+   bracketed by a CUDA event pair recorded on its launch stream, and lra_batch runs its groups
+   in order on one stream (no concurrent groups), so each interval is that kernel's own device
+   time (an isolation pass; the overlapped schedule is timed with profiling disabled).  lra_profile_read synchronizes
    on the recorded events, aggregates per kernel name (name -> total ms, launch count; at most
    cap names, written to host arrays) and resets the record; returns the number of names or a
    negative lra_status.  Enabling resets the record. */

@@ -93,7 +93,8 @@ def fourier_recursive(n: int, d: int) -> np.ndarray:
 def fourier_column_support(n: int, d: int, sigma: int):
     """Closed form of column σ of Ω_{n,d} (pinned against fourier_recursive):
     rows 2^d·(σ mod s) + t, t = 0..2^d−1, values ω_n^{tσ} (exponent reduced mod n
-    in integers before the trig call)."""
+    in integers before the trig call), evaluated as cos(a) + i sin(a) with a = fl(fl(2π e)/n)
+    — DESIGN.md reading C32 (one fixed faithful rounding of ω_n^e)."""
     s = n >> d
     q = 1 << d
     t = np.arange(q)

@@ -1094,12 +1094,10 @@ static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   CAArgs r = a;
   r.y_complex = 0;
   if (a.y_complex) r.Y = nullptr;
-  static const bool use_old = getenv("LRA_CA_OLD") != nullptr;   // A/B switch (diagnostics)
-  if (!use_old) {                                                // cluster tier, ca_cluster.cu
-    e = launch_ca_cluster(r, nb, maxN, st, cs_out, pf);
-    if (e != cudaErrorInvalidConfiguration) return e;
-    cudaGetLastError();
-  }
+  // cluster tier (ca_cluster.cu, q <= 48); k_ca's cluster form below covers 48 < q <= 64
+  e = launch_ca_cluster(r, nb, maxN, st, cs_out, pf);
+  if (e != cudaErrorInvalidConfiguration) return e;
+  cudaGetLastError();
   if (pick_cluster(maxN, NT / TPR, a.qp, a.q, Q, false, cs, rpc)) {   // cluster tier
     r.cs = cs;
     r.rpc = rpc;

@@ -1038,11 +1038,20 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   // Group size: as many problems as the cluster tier runs concurrently (one wave of co-resident
   // clusters; 7 for config 2 on a B200), so that one group's C-A fills the GPCs while the
   // previous group's nucleus / residual use the remaining SMs.  LRA_BATCH_GROUPS overrides.
+  // The grid and global-memory tiers use the handle's single exchange / C-matrix buffers and
+  // occupy every SM (cooperative grids), so their groups run in order on ONE side stream.
+  const int64_t maxN = m > n ? m : n;
+  if (cplx && ca_needs_global(maxN, (int)k))
+    return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
+  const int act = ca_needs_global(maxN, (int)k) ? 0 : ca_cluster_max_active(maxN, (int)k);
+  // While profiling (lra_profile_enable), the groups also run in order on one stream: every
+  // kernel's event interval is then its own device time, not time spent queued behind
+  // another group's kernels (the isolation pass of bench.py).
+  const int nside = (act >= 1 && !h->prof.on) ? LRA_NSIDE : 1;
   int64_t ngroups;
   if (h->groups_env > 0) {
     ngroups = nb < h->groups_env ? nb : h->groups_env;
   } else {
-    const int act = ca_cluster_max_active(m > n ? m : n, (int)k);
     const int64_t per = act >= 2 ? act : 4;
     ngroups = (nb + per - 1) / per;
     if (ngroups < 1) ngroups = 1;
@@ -1053,11 +1062,24 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   if ((s = resolve_mult(h, M0, n, st, &Mres)) != LRA_OK) return s;
   M0 = &Mres;
   CK(cudaEventRecord(h->fork, st));
-  for (int i = 0; i < LRA_NSIDE; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));
+  for (int i = 0; i < nside; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));
+  // Every exit after the fork joins the side streams back into `stream` (so a captured graph
+  // stays joined and later work on `stream` is ordered after everything enqueued here).
+  struct Join {
+    lra_handle h;
+    cudaStream_t st;
+    int n;
+    ~Join() {
+      for (int i = 0; i < n; ++i) {
+        cudaEventRecord(h->join[i], h->side[i]);
+        cudaStreamWaitEvent(st, h->join[i], 0);
+      }
+    }
+  } join{h, st, nside};
   const size_t wsz = W0->dtype == LRA_F32 ? 4 : 8;
   for (int64_t g = 0; g < ngroups; ++g) {
     const int64_t b0 = g * gsz, gn = (nb - b0) < gsz ? (nb - b0) : gsz;
-    cudaStream_t gs = h->side[g % LRA_NSIDE];
+    cudaStream_t gs = h->side[g % nside];
     lra_operand Wg = *W0;
     Wg.w = (const char *)W0->w + b0 * w_stride * wsz;
     lra_multiplier Mg = *M0;
@@ -1099,10 +1121,6 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
       CK(launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof));
     }
     h->launches += nl;
-  }
-  for (int i = 0; i < LRA_NSIDE; ++i) {
-    CK(cudaEventRecord(h->join[i], h->side[i]));
-    CK(cudaStreamWaitEvent(st, h->join[i], 0));
   }
   return LRA_OK;
 }

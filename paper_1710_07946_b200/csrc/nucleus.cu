@@ -13,7 +13,6 @@
 
 namespace lra {
 
-constexpr int NUC_NT = 1024;
 __device__ unsigned long long g_nuc_cnt[2];   // diagnostics: Jacobi sweeps, rotations (all problems)   // max threads; launched with 32 x (l/2) so each pair has a warp
 
 
@@ -28,15 +27,13 @@ __device__ __forceinline__ void rr_pair(int L, int round, int i, int &a, int &b)
   }
 }
 
-// KU = ceil(k / 32) (k = the long side); OLD = the reference pair loop (one warp per pair),
-// kept for the bit-identity check (env LRA_NUC_OLD).  The default loop gives each pair PL = 8
-// lanes and reproduces the warp-wide dot product bit for bit: lane h holds the partials that
+// KU = ceil(k / 32) (k = the long side).  Each pair gets PL lanes; the loop reproduces the warp-wide dot product bit for bit: lane h holds the partials that
 // lanes h, h+8, h+16, h+24 of a full warp held (same element order), adds them in the order of
 // the xor-16 and xor-8 butterfly levels, then finishes with xor 4, 2, 1 — the same sums in the
 // same association, so every rotation, and the whole SVD, is unchanged while a round issues a
 // quarter of the warps (the round was fp64-issue-bound with one warp per pair).
-template <int KU, bool OLD, int PL, int KC = 0>
-__global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
+template <int KU, int PL, int KC = 0>
+__global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
   const int NT = blockDim.x, NW = NT >> 5;
   extern __shared__ __align__(16) double nsm[];
   const int64_t b = blockIdx.x;
@@ -94,145 +91,93 @@ __global__ void __launch_bounds__(OLD ? NUC_NT : 512) k_nucleus(NucArgs a) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
     int rot = 0;
-    if constexpr (OLD) {
-      for (int round = 0; round < L - 1; ++round) {
-        for (int pi = warp; pi < L / 2; pi += NW) {
-          const int p = s_pair[2 * (round * (L / 2) + pi)], qq = s_pair[2 * (round * (L / 2) + pi) + 1];
-          double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
-          double xv[4], yv[4];
-          double ga = 0.0;
-  #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = lane + 32 * u;
-            xv[u] = i < k ? gp[i] : 0.0;
-            yv[u] = i < k ? gq[i] : 0.0;
-            ga = fma(xv[u], yv[u], ga);
-          }
-          ga = warp_sum(ga);
-          const double al = nrm[p], be = nrm[qq];
-          if (ga * ga > eps2 * al * be && ga != 0.0) {
-            const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
-            const double z2 = fma(zeta, zeta, 1.0);
-            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused;
-            // t -> 1 / (2 zeta) once zeta^2 overflows, t = 0 for a non-finite zeta (degenerate pairs:
-            // a column at rounding level, ga below the reciprocal's range)
-            const double t = z2 < INFINITY ? copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta)
-                                           : (isfinite(zeta) ? 0.5 / zeta : 0.0);
-            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
-  #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i = lane + 32 * u;
-              if (i < k) {
-                gp[i] = fma(cs, xv[u], -__dmul_rn(sn, yv[u]));
-                gq[i] = fma(sn, xv[u], __dmul_rn(cs, yv[u]));
-              }
-            }
-            double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
-            for (int u = 0; u < 4; ++u) {
-              const int i = lane + 32 * u;
-              if (i < L) {
-                const double x = vp[i], y = vq[i];
-                vp[i] = fma(cs, x, -__dmul_rn(sn, y));
-                vq[i] = fma(sn, x, __dmul_rn(cs, y));
-              }
-            }
-            if (lane == 0) {
-              nrm[p] = fma(-t, ga, al);
-              nrm[qq] = fma(t, ga, be);
-            }
-            rot = 1;
-            if (lane == 0) atomicAdd(&g_nuc_cnt[1], 1ull);
+    {
+    constexpr int GPW = 32 / PL, C = 32 / PL;   // pairs per warp, full-warp lanes per lane
+    constexpr int EV = (32 * KU) / PL;            // V elements per lane (L <= 32 KU)
+    const int grp = lane / PL, hl = lane % PL;
+    const unsigned gmask = 0xffffffffu;
+    for (int round = 0; round < L - 1; ++round) {
+      for (int base = warp * GPW; base < L / 2; base += NW * GPW) {   // warp-uniform trip count
+        const int pi = base + grp;
+        const bool act = pi < L / 2;
+        int p = 0, qq = 1;
+        if (act) {
+          p = s_pair[2 * (round * (L / 2) + pi)];
+          qq = s_pair[2 * (round * (L / 2) + pi) + 1];
+        }
+        double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
+        double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
+        double xs[C][KU], ys[C][KU], vx[EV], vy[EV], v[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {            // full-warp lane l = hl + PL c
+#pragma unroll
+          for (int u = 0; u < KU; ++u) {
+            const int i = hl + PL * c + 32 * u;
+            xs[c][u] = i < k ? gp[i] : 0.0;
+            ys[c][u] = i < k ? gq[i] : 0.0;
           }
         }
-        __syncthreads();
-      }
-    } else {
-      constexpr int GPW = 32 / PL, C = 32 / PL;   // pairs per warp, full-warp lanes per lane
-      constexpr int EV = (32 * KU) / PL;            // V elements per lane (L <= 32 KU)
-      const int grp = lane / PL, hl = lane % PL;
-      const unsigned gmask = 0xffffffffu;
-      for (int round = 0; round < L - 1; ++round) {
-        for (int base = warp * GPW; base < L / 2; base += NW * GPW) {   // warp-uniform trip count
-          const int pi = base + grp;
-          const bool act = pi < L / 2;
-          int p = 0, qq = 1;
-          if (act) {
-            p = s_pair[2 * (round * (L / 2) + pi)];
-            qq = s_pair[2 * (round * (L / 2) + pi) + 1];
-          }
-          double *gp = G + (size_t)p * ldg, *gq = G + (size_t)qq * ldg;
-          double *vp = V + (size_t)p * L, *vq = V + (size_t)qq * L;
-          double xs[C][KU], ys[C][KU], vx[EV], vy[EV], v[C];
 #pragma unroll
-          for (int c = 0; c < C; ++c) {            // full-warp lane l = hl + PL c
+        for (int e = 0; e < EV; ++e) {           // independent of the rotation: load early
+          const int i = hl + PL * e;
+          vx[e] = i < L ? vp[i] : 0.0;
+          vy[e] = i < L ? vq[i] : 0.0;
+        }
+        const double al = nrm[p], be = nrm[qq];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int u = 0; u < KU; ++u) acc = fma(xs[c][u], ys[c][u], acc);
+          v[c] = acc;
+        }
+#pragma unroll
+        for (int o = 16; o >= PL; o >>= 1) {     // butterfly levels held inside the lane
+          const int d = o / PL;
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if ((c & d) == 0 && c + d < C) v[c] = v[c] + v[c + d];
+        }
+        double ga = v[0];
+#pragma unroll
+        for (int o = PL / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o);
+        if (act && ga * ga > eps2 * al * be && ga != 0.0) {
+          const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
+          const double z2 = fma(zeta, zeta, 1.0);
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused;
+          // t -> 1 / (2 zeta) once zeta^2 overflows, t = 0 for a non-finite zeta (degenerate pairs:
+          // a column at rounding level, ga below the reciprocal's range)
+          const double t = z2 < INFINITY ? copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta)
+                                         : (isfinite(zeta) ? 0.5 / zeta : 0.0);
+          const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
               const int i = hl + PL * c + 32 * u;
-              xs[c][u] = i < k ? gp[i] : 0.0;
-              ys[c][u] = i < k ? gq[i] : 0.0;
+              if (i < k) {
+                gp[i] = fma(cs, xs[c][u], -__dmul_rn(sn, ys[c][u]));
+                gq[i] = fma(sn, xs[c][u], __dmul_rn(cs, ys[c][u]));
+              }
             }
           }
 #pragma unroll
-          for (int e = 0; e < EV; ++e) {           // independent of the rotation: load early
+          for (int e = 0; e < EV; ++e) {
             const int i = hl + PL * e;
-            vx[e] = i < L ? vp[i] : 0.0;
-            vy[e] = i < L ? vq[i] : 0.0;
-          }
-          const double al = nrm[p], be = nrm[qq];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            double acc = 0.0;
-#pragma unroll
-            for (int u = 0; u < KU; ++u) acc = fma(xs[c][u], ys[c][u], acc);
-            v[c] = acc;
-          }
-#pragma unroll
-          for (int o = 16; o >= PL; o >>= 1) {     // butterfly levels held inside the lane
-            const int d = o / PL;
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-              if ((c & d) == 0 && c + d < C) v[c] = v[c] + v[c + d];
-          }
-          double ga = v[0];
-#pragma unroll
-          for (int o = PL / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o);
-          if (act && ga * ga > eps2 * al * be && ga != 0.0) {
-            const double zeta = (be - al) * (0.5 * __drcp_rn(ga));
-            const double z2 = fma(zeta, zeta, 1.0);
-            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), sqrt(1 + zeta^2) = z2 * rsqrt(z2) fused;
-            // t -> 1 / (2 zeta) once zeta^2 overflows, t = 0 for a non-finite zeta (degenerate pairs:
-            // a column at rounding level, ga below the reciprocal's range)
-            const double t = z2 < INFINITY ? copysign(__drcp_rn(fma(z2, rsqrt(z2), fabs(zeta))), zeta)
-                                           : (isfinite(zeta) ? 0.5 / zeta : 0.0);
-            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-#pragma unroll
-              for (int u = 0; u < KU; ++u) {
-                const int i = hl + PL * c + 32 * u;
-                if (i < k) {
-                  gp[i] = fma(cs, xs[c][u], -__dmul_rn(sn, ys[c][u]));
-                  gq[i] = fma(sn, xs[c][u], __dmul_rn(cs, ys[c][u]));
-                }
-              }
+            if (i < L) {
+              vp[i] = fma(cs, vx[e], -__dmul_rn(sn, vy[e]));
+              vq[i] = fma(sn, vx[e], __dmul_rn(cs, vy[e]));
             }
-#pragma unroll
-            for (int e = 0; e < EV; ++e) {
-              const int i = hl + PL * e;
-              if (i < L) {
-                vp[i] = fma(cs, vx[e], -__dmul_rn(sn, vy[e]));
-                vq[i] = fma(sn, vx[e], __dmul_rn(cs, vy[e]));
-              }
-            }
-            if (hl == 0) {
-              nrm[p] = fma(-t, ga, al);
-              nrm[qq] = fma(t, ga, be);
-            }
-            rot = 1;
           }
+          if (hl == 0) {
+            nrm[p] = fma(-t, ga, al);
+            nrm[qq] = fma(t, ga, be);
+          }
+          rot = 1;
         }
-        __syncthreads();
       }
+      __syncthreads();
+    }
     }
     if (rot && lane == 0) atomicOr(&s_rot, 1);
     __syncthreads();
@@ -423,48 +368,38 @@ __global__ void __launch_bounds__(128) k_factor_B(FacArgs a) {
 
 cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf) {
   const size_t smem = nucleus_smem(na.k, na.l);
-  static const bool old = getenv("LRA_NUC_OLD") != nullptr;   // reference pair loop (diagnostics)
   static const int pl_env = getenv("LRA_NUC_PL") ? atoi(getenv("LRA_NUC_PL")) : 0;
   const int kl = na.k > na.l ? na.k : na.l, ku = (kl + 31) / 32;
   // lanes per pair (measured on B200: 16 fastest for k <= 64 and k > 96, 32 for 64 < k <= 96)
   const int PLs = pl_env == 8 || pl_env == 16 || pl_env == 32 ? pl_env : (ku == 3 ? 32 : 16);
   using KF = void (*)(NucArgs);
-  static const KF tab[4][4] = {
-      {k_nucleus<1, true, 32>, k_nucleus<2, true, 32>, k_nucleus<3, true, 32>, k_nucleus<4, true, 32>},
-      {k_nucleus<1, false, 8>, k_nucleus<2, false, 8>, k_nucleus<3, false, 8>, k_nucleus<4, false, 8>},
-      {k_nucleus<1, false, 16>, k_nucleus<2, false, 16>, k_nucleus<3, false, 16>, k_nucleus<4, false, 16>},
-      {k_nucleus<1, false, 32>, k_nucleus<2, false, 32>, k_nucleus<3, false, 32>, k_nucleus<4, false, 32>}};
-  const int row = old ? 0 : (PLs == 8 ? 1 : PLs == 16 ? 2 : 3);
+  static const KF tab[3][4] = {
+      {k_nucleus<1, 8>, k_nucleus<2, 8>, k_nucleus<3, 8>, k_nucleus<4, 8>},
+      {k_nucleus<1, 16>, k_nucleus<2, 16>, k_nucleus<3, 16>, k_nucleus<4, 16>},
+      {k_nucleus<1, 32>, k_nucleus<2, 32>, k_nucleus<3, 32>, k_nucleus<4, 32>}};
+  const int row = PLs == 8 ? 0 : PLs == 16 ? 1 : 2;
   KF kern = tab[row][ku - 1];
-  static const bool generic = getenv("LRA_NUC_GENERIC") != nullptr;   // diagnostics
-  static const int kcpl = getenv("LRA_NUC_KCPL") ? atoi(getenv("LRA_NUC_KCPL")) : 16;   // diagnostics
   int PLk = PLs;
-  if (!old && !generic && pl_env == 0 && na.k == na.l) {   // square shapes of the BASELINE configs
+  if (pl_env == 0 && na.k == na.l) {   // square shapes of the BASELINE configs (bounds fold)
     if (na.k == 48) {
-      PLk = kcpl;
-      kern = kcpl == 8 ? k_nucleus<2, false, 8, 48> : kcpl == 32 ? k_nucleus<2, false, 32, 48> : k_nucleus<2, false, 16, 48>;
+      kern = k_nucleus<2, 16, 48>;
     } else if (na.k == 20) {
-      kern = k_nucleus<1, false, 16, 20>;
+      kern = k_nucleus<1, 16, 20>;
     } else if (na.k == 8) {
-      kern = k_nucleus<1, false, 16, 8>;
+      kern = k_nucleus<1, 16, 8>;
     } else if (na.k == 96) {
-      kern = k_nucleus<3, false, 32, 96>;
+      kern = k_nucleus<3, 32, 96>;
+      PLk = 32;
     }
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   pf->begin("k_nucleus", st);
   const int L = ((na.k < na.l ? na.k : na.l) + 1) & ~1;
-  int nt;
-  if (old) {
-    nt = (L / 2) * 32 < 128 ? 128 : (L / 2) * 32;
-    if (nt > 1024) nt = 1024;
-  } else {
-    const int gpw = 32 / PLk;               // pairs per warp
-    nt = ((L / 2 + gpw - 1) / gpw) * 32;
-    if (nt < 256) nt = 256;
-    if (nt > 512) nt = 512;                 // the pair loop strides over the rest
-  }
+  const int gpw = 32 / PLk;                 // pairs per warp
+  int nt = ((L / 2 + gpw - 1) / gpw) * 32;
+  if (nt < 256) nt = 256;
+  if (nt > 512) nt = 512;                   // the pair loop strides over the rest
   kern<<<(unsigned)nb, nt, smem, st>>>(na);
   pf->end(st);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -942,3 +942,52 @@ def test_config2_batch_in_bench_configuration(P, h):
         assert list(bufs.J[b].cpu().numpy()) == list(ora.J)
         rho = float(np.sqrt(bufs.num2[b].item() / bufs.den2[b].item()))
         assert abs(rho / ora.rho - 1) <= 1e-4, (b, rho, ora.rho)
+
+
+def _batch_vs_oracle(P, h, Ws, mult, r, k, sweeps):
+    from paper_1710_07946_b200 import pipeline
+    nb = len(Ws)
+    Wt = torch.from_numpy(np.ascontiguousarray(np.stack([W.T for W in Ws]))).cuda()
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), P.lra.Multiplier(mult), r, k, sweeps, nb)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)
+    assert np.all(st["status"] == 0)
+    for b in range(nb):
+        ora = O.cur_pipeline(Ws[b], mult, r, k, k, sweeps)
+        assert list(bufs.I[b].cpu().numpy()) == list(ora.I), b
+        assert list(bufs.J[b].cpu().numpy()) == list(ora.J), b
+        assert st["swaps"][b] == ora.ca.swaps, b
+
+
+def test_batch_grid_tier_all_blocks_vs_oracle(P, h):
+    """lra_batch whose blocks exceed the cluster tier (4608 x 512, k = 32: 4608 rows > 16 CTAs
+    x 256 rows) runs the grid tier, which shares the handle's exchange buffer: its groups run
+    in order on one side stream.  All 8 blocks equal the oracle (pivots, swaps)."""
+    Ws = [synth.factor_gaussian(700 + i, 4608, 512, 24, 1e-12).astype(np.float32) for i in range(8)]
+    mult = synth.multiplier_abridged(3, 512, 3, 32, "arht")
+    _batch_vs_oracle(P, h, Ws, mult, 24, 32, 2)
+
+
+def test_batch_forced_global_tier_all_blocks_vs_oracle():
+    """lra_batch with the global-memory tier forced (LRA_CA_FORCE_GLOBAL=1, subprocess) over 8
+    blocks: the tier's single C-matrix scratch is used by one group at a time, so
+    every block equals the oracle (pivots, swaps)."""
+    out = _run_forced_global(
+        "import json, numpy as np, torch, synth\n"
+        "from paper_1710_07946_b200 import Handle, lra, pipeline\n"
+        "Ws = [synth.factor_gaussian(800 + i, 1024, 768, 12, 1e-12).astype(np.float32) for i in range(8)]\n"
+        "M = synth.multiplier_abridged(5, 768, 2, 16, 'arht')\n"
+        "Wt = torch.from_numpy(np.ascontiguousarray(np.stack([W.T for W in Ws]))).cuda()\n"
+        "h = Handle(0); b = pipeline.cur_batch(h, lra.Dense(Wt), lra.Multiplier(M), 12, 16, 2, 8)\n"
+        "torch.cuda.synchronize(); st = lra.stats_to_numpy(b.stats)\n"
+        "print(json.dumps({'I': b.I.cpu().tolist(), 'J': b.J.cpu().tolist(), 'swaps': st['swaps'].tolist(),"
+        " 'status': st['status'].tolist()}))\n")
+    import json
+    g = json.loads(out.strip().splitlines()[-1])
+    M = synth.multiplier_abridged(5, 768, 2, 16, "arht")
+    for b in range(8):
+        W = synth.factor_gaussian(800 + b, 1024, 768, 12, 1e-12).astype(np.float32)
+        ora = O.cur_pipeline(W, M, 12, 16, 16, 2)
+        assert g["status"][b] == 0
+        assert g["I"][b] == list(ora.I) and g["J"][b] == list(ora.J), b
+        assert g["swaps"][b] == ora.ca.swaps, b

@@ -271,6 +271,28 @@ def test_certificate_holds_and_vanishes():
     assert b0 == 0.0
 
 
+def test_certificate_hand_evaluated_eqnrm11():
+    """Two-sided pin of eq. (eqnrm11), on hand-evaluated cases (Frobenius norm,
+    mu = 1, (1 - theta) xi = sqrt(kl), theta = ||U|| eta Delta with ||U|| <= ||U||_F, C27).
+
+    Case 1: C = ones(4,2), R = ones(2,4), U = I_2, k = l = r = 2 (eta = 1), Delta = 0.01:
+      |C| = |R| = sqrt 8, |U| = sqrt 2, theta = 0.01 sqrt 2 = 0.0141421356...,
+      xi = 2 / (1 - theta) = 2.02869000924931...,
+      bound = 0.01 ((2 sqrt 8 + 0.01 + 8 sqrt 2) xi sqrt 2 + 1) = 0.497172502312...
+    Case 2: C = ones(4,3), R = ones(3,4), U = I_3 / 2, k = l = 3, r = 2 (eta = 2), Delta = 0.05:
+      |C| = |R| = sqrt 12, |U| = sqrt 3 / 2, theta = 2 (0.05) sqrt 3 / 2 = 0.0866025403...,
+      xi = 3 / (1 - theta), bound = 0.05 ((2 sqrt 12 + 0.05 + 2 (12) sqrt 3 / 2) xi sqrt 3 / 2 + 1)
+           = 3.99844013691766...
+    Case 3: theta >= 1 (|U| eta Delta = 2 sqrt 2 * 0.5 > 1): no certificate (inf)."""
+    b1, nc, nr, nu = lra.cur_certificate(np.ones((4, 2)), np.ones((2, 4)), np.eye(2), 2, 0.01)
+    assert b1 == pytest.approx(0.49717250231232796, rel=1e-13, abs=0)
+    assert (nc, nr, nu) == pytest.approx((8 ** 0.5, 8 ** 0.5, 2 ** 0.5), rel=1e-15)
+    b2, *_ = lra.cur_certificate(np.ones((4, 3)), np.ones((3, 4)), 0.5 * np.eye(3), 2, 0.05)
+    assert b2 == pytest.approx(3.9984401369176634, rel=1e-13, abs=0)
+    b3, *_ = lra.cur_certificate(np.ones((4, 2)), np.ones((2, 4)), 2 * np.eye(2), 2, 0.5)
+    assert b3 == float("inf")
+
+
 def test_progressive_depth_stops_at_first_passing_depth():
     """d = 1 already passes on a generic perturbed low-rank input; an impossible
     tolerance runs to dmax; the estimate is the sampled ratio."""
