@@ -173,12 +173,10 @@ def _oracle_cfg3(n_blocks, seed):
     from oracle import lra as O
     s, t = synth.cauchy_params(seed, n_blocks, C3_M, C3_M)
     mult = synth.multiplier_sparse_batch(seed, n_blocks, C3_M, C3_K)
-    per = C3_K * 4
     Ws = [synth.cauchy_block(s[b], t[b]) for b in range(n_blocks)]
     t0 = time.perf_counter()
     for b in range(n_blocks):
-        mb = {"kind": "sparse", "lbar": C3_K, "nnz": 4, "sp_row": mult["sp_row"][b * per:(b + 1) * per],
-              "sp_sign": mult["sp_sign"][b * per:(b + 1) * per]}
+        mb = dict(mult, sp_row=mult["sp_row"][b], sp_sign=mult["sp_sign"][b])
         O.cur_pipeline(Ws[b], mb, C3_R, C3_K, C3_K, C3_T)
     return time.perf_counter() - t0
 
@@ -415,10 +413,7 @@ def run_cfg3(h, ws, rank, steps, warmup, peaks, src):
     s, t = synth.cauchy_params(0, C3_NB, C3_M, C3_M)
     Wt = synth.cauchy_blocks_torch(s[b0:b0 + per], t[b0:b0 + per], "cuda")
     mult = synth.multiplier_sparse_batch(0, C3_NB, C3_M, C3_K)
-    nnz = C3_K * 4
-    mb = dict(mult)
-    mb["sp_row"] = mult["sp_row"][b0 * nnz:(b0 + per) * nnz]
-    mb["sp_sign"] = mult["sp_sign"][b0 * nnz:(b0 + per) * nnz]
+    mb = dict(mult, sp_row=mult["sp_row"][b0:b0 + per], sp_sign=mult["sp_sign"][b0:b0 + per], nb=per)
     M = lra.Multiplier(mb)
     W = lra.Dense(Wt)
     bufs = pipeline.BatchBuffers(per, C3_R, C3_K)

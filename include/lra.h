@@ -108,12 +108,14 @@ typedef struct {
   double cert_cols;         /* max |C'| at exit of the last horizontal step (<= 1 + tol)     */
 } lra_ca_stats;
 
-/* Precision of the reconstruction A*B inside the full a-posteriori pass (DESIGN.md §6).
+/* Precision of the reconstruction A*B inside the full a-posteriori pass (DESIGN.md §6.2).
    Both run the product on the tcgen05 tensor cores as an exact int8 digit-slice
-   (Ozaki-style) contraction with int32 TMEM accumulators, recombined in fp64:
-   PRECISE uses 6 slices per operand (truncation ~2^-42 of max|A_i| max|B_j| r, enough for
-   rho ~ 1e-8 on fp32 W), FAST 3 slices (~2^-21, fp32-class).  fp64 W in PRECISE mode uses
-   an fp64 FMA kernel instead (fp64-exact to rounding). */
+   (Ozaki-style) contraction with int32 TMEM accumulators, recombined exactly in int64:
+   balanced base-256 digits, one exponent per row of A and per 32/64-column tile of B.
+   PRECISE keeps 6 slices per operand (levels s + u <= 5: truncation ~2^-45 of
+   max|A_i| max|B_j|; rho within ~1e-8 of the exact product on configs 2 and 3), FAST 3
+   slices (~2^-21, fp32-class).  fp64 W in PRECISE mode, or a configuration the tensor-core
+   kernel cannot hold (r > 64 in PRECISE), uses an fp64 FMA kernel (fp64-exact to rounding). */
 typedef enum {
   LRA_RECON_FAST = 0,
   LRA_RECON_PRECISE = 1

@@ -7,11 +7,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SO = os.path.join(HERE, "liblra.so")
+SO = os.environ.get("LRA_BUILD_OUT") or os.path.join(HERE, "liblra.so")   # LRA_BUILD_OUT: diagnostic builds
 SOURCES = ["lra_api.cu", "sketch.cu", "ca.cu", "ca_cluster.cu", "ca_global.cu", "nucleus.cu", "residual.cu", "residual_tc.cu", "shard.cu", "expand.cu", "qrp.cu", "leverage.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"] + os.environ.get("LRA_EXTRA_FLAGS", "").split()
 
 
 def _stale() -> bool:
@@ -29,7 +29,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     from concurrent.futures import ThreadPoolExecutor
 
     def compile_one(src):
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(CSRC, src.replace(".cu", (os.environ.get("LRA_OBJ_TAG", "") + ".o")))
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 

@@ -257,9 +257,9 @@ static lra_status resolve_mult(lra_handle h, const lra_multiplier *M, int64_t n,
   return LRA_OK;
 }
 
-// Reconstruction path of the full residual (DESIGN.md §6): fp32 W (or FAST) -> tensor-core
-// Ozaki kernel with S = 6 (PRECISE) / 3 (FAST) int8 digit slices; fp64 W in PRECISE mode ->
-// fp64 SIMT kernel.  LRA_RESID_SIMT=1 forces the SIMT kernel (A/B diagnostics).
+// Reconstruction path of the full residual (DESIGN.md §6.2): fp32 W (or FAST) -> tensor-core
+// Ozaki kernel with S = 6 (PRECISE) / 3 (FAST) balanced base-256 digit slices; fp64 W in
+// PRECISE mode -> fp64 SIMT kernel.  LRA_RESID_SIMT=1 forces the SIMT kernel (diagnostics).
 static int resid_slices(int dtype, int prec) {
   static const bool simt = getenv("LRA_RESID_SIMT") != nullptr;
   if (prec == LRA_RECON_FAST) return 3;
@@ -780,12 +780,16 @@ lra_status lra_cur_residual(lra_handle h, const lra_operand *W, const double *A,
   a.partial = (double2 *)h->ws;
   a.status = nullptr;
   int nl = 0;
+  cudaError_t e = cudaErrorInvalidConfiguration;
   if (S) {
     char *tcs = (char *)h->ws + (((size_t)resid_partials(W->m, W->n) * sizeof(double2) + 255) & ~(size_t)255);
-    CK(launch_residual_tc(a, 1, S, tcs, num2, den2, st, &nl, &h->prof));
-  } else {
-    CK(launch_residual(a, 1, num2, den2, st, &nl, &h->prof));
+    e = launch_residual_tc(a, 1, S, tcs, num2, den2, st, &nl, &h->prof);
   }
+  if (e == cudaErrorInvalidConfiguration) {   // no tensor-core configuration for this r: fp64 SIMT pass
+    cudaGetLastError();
+    e = launch_residual(a, 1, num2, den2, st, &nl, &h->prof);
+  }
+  CK(e);
   if (W->m_global > 0) {   // row-sharded: sum the partial norms over the ranks
     if ((s = allreduce_sum(h, num2, 1, st)) != LRA_OK) return s;
     if ((s = allreduce_sum(h, den2, 1, st)) != LRA_OK) return s;
@@ -1113,13 +1117,17 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
     ra.partial = part + b0 * tiles;
     ra.status = status + b0;
     int nl = 0;
+    cudaError_t e = cudaErrorInvalidConfiguration;
     if (S) {   // each group uses its own slice of the tensor-core scratch
       char *g_tcs = tcs + (residual_tc_scratch(m, n, (int)r, S, nb) - 1024) / nb * b0;
       g_tcs = (char *)(((uintptr_t)g_tcs + 255) & ~(uintptr_t)255);
-      CK(launch_residual_tc(ra, gn, S, g_tcs, num2 + b0, den2 + b0, gs, &nl, &h->prof));
-    } else {
-      CK(launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof));
+      e = launch_residual_tc(ra, gn, S, g_tcs, num2 + b0, den2 + b0, gs, &nl, &h->prof);
     }
+    if (e == cudaErrorInvalidConfiguration) {   // fp64 SIMT pass (fp64 W PRECISE, or r beyond the TC tiles)
+      cudaGetLastError();
+      e = launch_residual(ra, gn, num2 + b0, den2 + b0, gs, &nl, &h->prof);
+    }
+    CK(e);
     h->launches += nl;
   }
   return LRA_OK;

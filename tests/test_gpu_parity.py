@@ -283,7 +283,7 @@ def _residual_gpu(P, h, W, A, B, r, prec):
 
 def test_residual_tc_config2_oracle_factors(P, h):
     """a5 in isolation on BASELINE config 2 (fp32 4096², r = 32, rho ~ 7e-7): the tensor-core
-    int8 digit-slice product (PRECISE, 6 slices) reproduces the oracle's fp64 rho to 1e-6
+    int8 digit-slice product (PRECISE, 6 base-256 slices) reproduces the oracle's fp64 rho to 1e-6
     relative given the oracle's own A, B (so the only difference is the product arithmetic)."""
     W = synth.config2(0)
     M = synth.multiplier_abridged(0, 4096, 4, 48, "arht")
