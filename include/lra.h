@@ -325,6 +325,12 @@ lra_status lra_debug_counters(uint64_t *out16 /* host */, int reset);
    [8] tiles.  out16: host array of 16.  Synchronizes the device. */
 lra_status lra_debug_counters_residual(uint64_t *out16 /* host */, int reset);
 
+/* Diagnostics (builds with -DLRA_CHECK_IDX=1 only; zeros otherwise): the first out-of-range
+   data-dependent row / column index seen by a kernel: out4 (host) = { kernel id (1-2 nucleus
+   gather, 3-4 factor gathers, 5-6 C-A block gathers), problem, index, bound }; such an index is
+   clamped to 0.  Synchronizes the device.  reset != 0 clears the record. */
+lra_status lra_debug_index_errors(int64_t *out4 /* host */, int reset);
+
 /* Thread-local message for the last non-OK status (never NULL). */
 const char *lra_last_error(void);
 

@@ -450,8 +450,15 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
           if (e < tot) {
             const int i = e % nloc, j = e / nloc;
             if (kind == 0) v[u] = __ldg(Y + (int64_t)j * a.ldy + r0 + i);
-            else if (kind == 1) v[u] = op_at<OPK>(op, I[j], r0 + i);
-            else v[u] = op_at<OPK>(op, r0 + i, J[j]);
+            else if (kind == 1) {
+              long long ii = I[j];
+              LRA_CHKIDX(5, b, ii, op.m);
+              v[u] = op_at<OPK>(op, ii, r0 + i);
+            } else {
+              long long jj = J[j];
+              LRA_CHKIDX(6, b, jj, op.n);
+              v[u] = op_at<OPK>(op, r0 + i, jj);
+            }
           }
         }
 #pragma unroll
@@ -736,7 +743,8 @@ static cudaError_t launch_cc_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool cl1 = getenv("LRA_CA_CLUSTER1") != nullptr;   // diagnostics: cluster attribute for cs = 1
+  cfg.numAttrs = (cs > 1 || cl1) ? 1 : 0;
   pf->begin("k_ca", st);
   e = cudaLaunchKernelEx(&cfg, kern, a);
   pf->end(st);
@@ -793,6 +801,15 @@ cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t s
   if (a.q <= 32) return launch_cc_t<32, 2>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 48) return launch_cc_t<48, 2>(a, nb, maxN, st, cs_out, pf);
   return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t read_idx_err_cc(long long *out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_idx_err, sizeof(g_idx_err));
+  if (e == cudaSuccess && reset) {
+    long long z[4] = {0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_idx_err, z, sizeof(z));
+  }
+  return e;
 }
 
 cudaError_t read_cc_counters(unsigned long long *out, bool reset) {

@@ -10,6 +10,32 @@
 #define LRA_QMAX 64         // largest k = l handled by the on-chip (cluster / grid) tiers
 #define LRA_QMAX_ALL 112    // largest k = l handled at all (global-memory tier; the nucleus's H and V fit in shared memory)
 
+// ------------------------------------------------------- index checks (diagnostic builds)
+// Built with -DLRA_CHECK_IDX=1: data-dependent row / column indices are range-checked before
+// use; the first violation (kernel id, problem, index value, bound) is recorded in
+// lra::g_idx_err and the index is clamped so the kernel does not fault.
+#ifndef LRA_CHECK_IDX
+#define LRA_CHECK_IDX 0
+#endif
+namespace lra {
+static __device__ long long g_idx_err[4];   // one per translation unit (no relocatable device code)
+}
+#if LRA_CHECK_IDX
+#define LRA_CHKIDX(kid, prob, v, N)                                                            \
+  do {                                                                                         \
+    if ((v) < 0 || (v) >= (N)) {                                                               \
+      if (atomicCAS((unsigned long long *)&lra::g_idx_err[0], 0ull, (unsigned long long)(kid)) == 0ull) { \
+        lra::g_idx_err[1] = (long long)(prob);                                                 \
+        lra::g_idx_err[2] = (long long)(v);                                                    \
+        lra::g_idx_err[3] = (long long)(N);                                                    \
+      }                                                                                        \
+      (v) = 0;                                                                                 \
+    }                                                                                          \
+  } while (0)
+#else
+#define LRA_CHKIDX(kid, prob, v, N) do { } while (0)
+#endif
+
 // ----------------------------------------------------------------------------- complex
 struct cplx {
   double re, im;

@@ -78,6 +78,8 @@ cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t s
 size_t nucleus_smem(int k, int l);
 bool nucleus_fits(int k, int l);
 cudaError_t read_nuc_counters(unsigned long long *out, bool reset);
+cudaError_t read_idx_err_nuc(long long *out, bool reset);   // diagnostics (LRA_CHECK_IDX builds)
+cudaError_t read_idx_err_cc(long long *out, bool reset);
 cudaError_t read_cc_counters(unsigned long long *out, bool reset);
 int ca_cluster_max_active(int64_t maxN, int q);
 // global-memory tier (ca_global.cu): any N, q <= 128; scratch ca_global_scratch_bytes

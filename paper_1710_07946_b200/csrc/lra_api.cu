@@ -390,6 +390,15 @@ lra_status lra_debug_counters(uint64_t *out8, int reset) {
   return LRA_OK;
 }
 
+lra_status lra_debug_index_errors(int64_t *out4, int reset) {
+  if (!out4) return fail(LRA_EINVAL, "null output");
+  long long a[4], c[4];
+  CK(read_idx_err_nuc(a, reset != 0));
+  CK(read_idx_err_cc(c, reset != 0));
+  for (int i = 0; i < 4; ++i) out4[i] = a[0] ? a[i] : c[i];
+  return LRA_OK;
+}
+
 lra_status lra_debug_counters_residual(uint64_t *out16, int reset) {
   if (!out16) return fail(LRA_EINVAL, "null output");
   CK(read_rtc_counters((unsigned long long *)out16, reset != 0));

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
   double *V = G + (size_t)L * ldg;     // L x L
   double *sig = V + (size_t)L * L;     // L
   int *ord = reinterpret_cast<int *>(sig + L);
-  __shared__ int s_rot;
+  __shared__ int s_rot[2];   // rotation flag of sweep s in s_rot[s & 1] (double-buffered)
   OpView op = a.op;
   if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
   const int64_t *I = a.I + b * a.k, *J = a.J + b * a.l;
@@ -59,7 +59,14 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
   for (int e = tid; e < L * k; e += NT) {
     int j = e / k, i = e % k;          // H[i, j] = tr ? G[j, i] : G[i, j]
     const int gi = tr ? j : i, gj = tr ? i : j;
-    G[e] = j < l ? (a.Gd ? a.Gd[(size_t)b * k * l + (size_t)gj * a.k + gi] : op.at(I[gi], J[gj])) : 0.0;
+    long long ii = 0, jj = 0;
+    if (j < l && !a.Gd) {
+      ii = I[gi];
+      jj = J[gj];
+      LRA_CHKIDX(1, b, ii, op.m);
+      LRA_CHKIDX(2, b, jj, op.n);
+    }
+    G[e] = j < l ? (a.Gd ? a.Gd[(size_t)b * k * l + (size_t)gj * a.k + gi] : op.at(ii, jj)) : 0.0;
   }
   for (int e = tid; e < L * L; e += NT) V[e] = (e / L == e % L) ? 1.0 : 0.0;
   __syncthreads();
@@ -81,6 +88,7 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
   }
   const double eps = 4.0 * (double)k * 2.220446049250313e-16;
   const double eps2 = eps * eps;
+  if (tid == 0) s_rot[0] = s_rot[1] = 0;   // ordered before any use by the barrier after the norms
   for (int sweep = 0; sweep < 40; ++sweep) {
     for (int j = warp; j < L; j += NW) {
       double s2 = 0.0;
@@ -88,7 +96,6 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
       s2 = warp_sum(s2);
       if (lane == 0) nrm[j] = s2;
     }
-    if (tid == 0) s_rot = 0;
     __syncthreads();
     int rot = 0;
     {
@@ -179,10 +186,20 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
       __syncthreads();
     }
     }
-    if (rot && lane == 0) atomicOr(&s_rot, 1);
+    if (rot && lane == 0) atomicOr(&s_rot[sweep & 1], 1);
     __syncthreads();
-    if (tid == 0) atomicAdd(&g_nuc_cnt[0], 1ull);
-    if (!s_rot) break;
+    // Every thread reads this sweep's flag; the NEXT sweep's flag is cleared here, after the
+    // barrier that ends this sweep (all of its readers, in the previous sweep, are past it).
+    // (Round 1 reset a single flag at the top of the sweep: a fast warp could clear it before a
+    // slow warp had read it, the slow warp left the loop alone and the CTA desynchronised —
+    // caught by cuda-gdb as an out-of-range shared-memory address in the TS write under
+    // concurrent batch groups.)
+    const int any = s_rot[sweep & 1];
+    if (tid == 0) {
+      s_rot[(sweep + 1) & 1] = 0;
+      atomicAdd(&g_nuc_cnt[0], 1ull);
+    }
+    if (!any) break;
   }
   // singular values, descending order (ties: lower column first)
   for (int j = warp; j < L; j += NW) {
@@ -276,7 +293,9 @@ __global__ void __launch_bounds__(128) k_factor_A(FacArgs a) {
 #pragma unroll
       for (int y = 0; y < PF; ++y) {
         const int64_t i = i0 + 128 * x;
-        w[x][y] = (j0 + y < l && i < op.m) ? op.at(i, J[j0 + y]) : 0.0;
+        long long jj = (j0 + y < l && i < op.m) ? J[j0 + y] : 0;
+        LRA_CHKIDX(3, b, jj, op.n);
+        w[x][y] = (j0 + y < l && i < op.m) ? op.at(i, jj) : 0.0;
       }
 #pragma unroll
     for (int y = 0; y < PF; ++y) {
@@ -337,7 +356,9 @@ __global__ void __launch_bounds__(128) k_factor_B(FacArgs a) {
       for (int y = 0; y < PF; ++y) {
         const int s = s0 + y;
         const int64_t j = j0c + 128 * x;
-        w[x][y] = (s < k && j < op.n) ? (a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(I[s], j)) : 0.0;
+        long long ii = (s < k && j < op.n && !a.Rt) ? I[s] : 0;
+        LRA_CHKIDX(4, b, ii, op.m);
+        w[x][y] = (s < k && j < op.n) ? (a.Rt ? a.Rt[(int64_t)s * op.n + j] : op.at(ii, j)) : 0.0;
       }
 #pragma unroll
     for (int y = 0; y < PF; ++y) {
@@ -427,6 +448,15 @@ cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cud
   pf->end(st);
   *nlaunch += 3;
   return cudaGetLastError();
+}
+
+cudaError_t read_idx_err_nuc(long long *out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_idx_err, sizeof(g_idx_err));
+  if (e == cudaSuccess && reset) {
+    long long z[4] = {0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_idx_err, z, sizeof(z));
+  }
+  return e;
 }
 
 cudaError_t read_nuc_counters(unsigned long long *out, bool reset) {

@@ -119,6 +119,8 @@ def _load():
     lib.lra_debug_counters.restype = C.c_int
     lib.lra_debug_counters_residual.argtypes = [P(C.c_uint64), C.c_int]
     lib.lra_debug_counters_residual.restype = C.c_int
+    lib.lra_debug_index_errors.argtypes = [P(i64), C.c_int]
+    lib.lra_debug_index_errors.restype = C.c_int
     for f in ("lra_handle_create", "lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
         getattr(lib, f).restype = C.c_int
     return lib
@@ -136,7 +138,8 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_nccl_unique_id",
+            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_debug_index_errors",
+            "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
             "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns", "lra_contract_columns",
@@ -155,8 +158,15 @@ def debug_counters_residual(reset=True):
     out = (C.c_uint64 * 16)()
     _check(lib().lra_debug_counters_residual(out, int(reset)))
     names = ["mma_wait_b", "mma_wait_tmem", "mma_issue", "prod_wait_b", "prod_wait_a", "mma_wait_a",
-             "epi_wait_tmem", "epi_work", "tiles", "epi_ldtm", "epi_wait_w"]
+             "epi_wait_tmem", "epi_work", "tiles", "epi_wait_w", "prod_wait_w"]
     return dict(zip(names, [int(x) for x in out]))
+
+
+def debug_index_errors(reset=True):
+    """First out-of-range data-dependent index (LRA_CHECK_IDX builds): (kernel id, problem, value, bound)."""
+    out = (C.c_int64 * 4)()
+    _check(lib().lra_debug_index_errors(out, int(reset)))
+    return tuple(int(x) for x in out)
 
 
 def _check(st):

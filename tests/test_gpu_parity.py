@@ -991,3 +991,28 @@ def test_batch_forced_global_tier_all_blocks_vs_oracle():
         assert g["status"][b] == 0
         assert g["I"][b] == list(ora.I) and g["J"][b] == list(ora.J), b
         assert g["swaps"][b] == ora.ca.swaps, b
+
+
+def test_batch_concurrent_groups_repeated_deterministic(P, h):
+    """Regression (round 2): lra_batch over 1184 config-3 blocks = 8 groups of 148 on the 8 side
+    streams, 25 times.  Concurrent groups once exposed a shared-memory race in the Jacobi
+    nucleus (a reset of the sweep's rotation flag before a slow warp had read it), faulting
+    rarely; now every call completes, every block is OK and the results are identical call to
+    call (the arithmetic is deterministic, whatever the interleaving of the groups)."""
+    from paper_1710_07946_b200 import pipeline
+    nb = 1184
+    s, t = synth.cauchy_params(0, nb)
+    Wt = synth.cauchy_blocks_torch(s, t, "cuda")
+    M = P.lra.Multiplier(synth.multiplier_sparse_batch(0, nb, 512, 20))
+    bufs = pipeline.BatchBuffers(nb, 16, 20)
+    ref = None
+    for rep in range(25):
+        pipeline.cur_batch(h, P.lra.Dense(Wt), M, 16, 20, 2, nb, bufs=bufs)
+        torch.cuda.synchronize()
+        st = P.lra.stats_to_numpy(bufs.stats)
+        assert np.all(st["status"] == 0), rep
+        cur = (bufs.I.cpu().numpy().copy(), bufs.num2.cpu().numpy().copy(), bufs.den2.cpu().numpy().copy())
+        if ref is None:
+            ref = cur
+        else:
+            assert np.array_equal(cur[0], ref[0]) and np.array_equal(cur[1], ref[1]) and np.array_equal(cur[2], ref[2]), rep
