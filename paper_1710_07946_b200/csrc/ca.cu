@@ -529,6 +529,7 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
       Pick pk = exchange(c, p, Mc, idx, v, Q, 1, t);
       if (!(pk.M > 0.0) || !isfinite(pk.M)) return false;
       if (pk.amb) {                                  // exact second round (tie window)
+        if (threadIdx.x == 0 && c.rank == 0) atomicAdd(&g_ca_cyc[8], 1ull);
         const double thr = (1.0 - c.tau) * pk.M;
         unsigned u2 = (has && myslot < 0 && val >= thr) ? (unsigned)grow : 0xffffffffu;
         double v2 = val;
@@ -655,6 +656,7 @@ __device__ __forceinline__ bool maxvol_real(Ctx &c, int64_t N, long long *S, boo
       return true;
     }
     if (pk.amb) {
+      if (threadIdx.x == 0 && c.rank == 0) atomicAdd(&g_ca_cyc[8], 1ull);
       const double thr = (1.0 - c.tau) * pk.M;
       int j2 = Q;
       double v2 = 0.0;
@@ -1167,6 +1169,9 @@ cudaError_t read_ca_counters(unsigned long long *out, bool reset) {
   if (e == cudaSuccess) e = read_cc_counters(c2, reset);
   if (e == cudaSuccess)
     for (int i = 0; i < 16; ++i) out[i] += c2[i];
+  unsigned long long gx = 0;
+  if (e == cudaSuccess) e = read_gm_exact(&gx, reset);
+  if (e == cudaSuccess) out[8] += gx;          // exact second rounds of the global-memory tier
   unsigned long long nc[2];
   if (e == cudaSuccess) e = read_nuc_counters(nc, reset);
   if (e == cudaSuccess) { out[14] = nc[0]; out[15] = nc[1]; }

@@ -267,9 +267,12 @@ __device__ __forceinline__ void decide(Sh<Q> &sh, const Cand &cd, double tau, co
 
 // exact round: smallest linear index with value >= thr over the problem (per-thread value
 // supplied by the caller's pass as `mine`).
+__device__ unsigned long long g_gm_exact;   // exact second rounds (diagnostics)
+
 template <int Q>
 __device__ __forceinline__ unsigned decide_exact(Sh<Q> &sh, unsigned mine, const GmArgs &g, int &par) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_gm_exact, 1ull);
   const int p = par;
   par ^= 1;
   const unsigned wi = wminu(mine);
@@ -667,6 +670,15 @@ cudaError_t launch_ca_global(CAArgs a, int64_t nb, int64_t maxN, void *scratch, 
   if (a.q <= 96) return launch_gm_t<96, 16>(a, nb, maxN, scratch, st, pf);
   if (a.q <= 128) return launch_gm_t<128, 16>(a, nb, maxN, scratch, st, pf);
   return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t read_gm_exact(unsigned long long *out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, cgm::g_gm_exact, sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z = 0;
+    e = cudaMemcpyToSymbol(cgm::g_gm_exact, &z, sizeof(z));
+  }
+  return e;
 }
 
 }  // namespace lra

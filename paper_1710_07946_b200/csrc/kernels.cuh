@@ -81,6 +81,7 @@ cudaError_t read_nuc_counters(unsigned long long *out, bool reset);
 cudaError_t read_idx_err_nuc(long long *out, bool reset);   // diagnostics (LRA_CHECK_IDX builds)
 cudaError_t read_idx_err_cc(long long *out, bool reset);
 cudaError_t read_cc_counters(unsigned long long *out, bool reset);
+cudaError_t read_gm_exact(unsigned long long *out, bool reset);
 int ca_cluster_max_active(int64_t maxN, int q);
 // global-memory tier (ca_global.cu): any N, q <= 128; scratch ca_global_scratch_bytes
 size_t ca_global_scratch_bytes(int64_t maxN, int q);

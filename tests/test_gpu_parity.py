@@ -1016,3 +1016,53 @@ def test_batch_concurrent_groups_repeated_deterministic(P, h):
             ref = cur
         else:
             assert np.array_equal(cur[0], ref[0]) and np.array_equal(cur[1], ref[1]) and np.array_equal(cur[2], ref[2]), rep
+
+
+# ------------------------------------------------------------ tie rule (reading C11) on the GPU
+def _plant_ties(W, seed, npairs, axis):
+    """Copy npairs random rows (axis 0) or columns (axis 1) of W onto other random ones, half
+    exactly and half scaled by (1 + 3e-13) (inside the tie window tau = 1e-12): the copies
+    give exactly equal or within-tau pivot candidates in rows owned by different warps, CTAs
+    and cluster ranks."""
+    g = np.random.default_rng(seed)
+    n = W.shape[axis]
+    perm = g.permutation(n)
+    src, dst = perm[:npairs], perm[npairs:2 * npairs]
+    for t, (a, b) in enumerate(zip(src, dst)):
+        f = 1.0 if t % 2 == 0 else 1.0 + 3e-13
+        if axis == 0:
+            W[b, :] = W[a, :] * f
+        else:
+            W[:, b] = W[:, a] * f
+    return W
+
+
+@pytest.mark.parametrize("tier", ["cluster", "grid", "global"])
+def test_tie_rule_planted_ties_vs_oracle(P, tier):
+    """Reading C11 (smallest row-major index among |c| >= (1 - tau) max) on inputs with planted
+    exact and within-tau ties: rows / columns duplicated (and scaled by 1 + 3e-13) across the
+    matrix, so that pivot candidates tie between warps, CTAs and cluster ranks.  Cluster tier:
+    4096^2, k = 48 (16-CTA clusters); grid tier: 9000 x 600, k = 16 (18 cooperative CTAs);
+    global tier: 3000 x 2600, k = 96.  Pivots, swap counts equal the oracle bit for bit, and the
+    exact second round ran (the fast per-unit decision was ambiguous at least once)."""
+    h = P.Handle(0)
+    if tier == "cluster":
+        W, r, k, d = synth.factor_gaussian(31, 4096, 4096, 40, 1e-6), 32, 48, 4
+    elif tier == "grid":
+        W, r, k, d = synth.factor_gaussian(32, 9000, 600, 12, 1e-6), 12, 16, 3
+    else:
+        W, r, k, d = synth.factor_gaussian(33, 3000, 2600, 80, 1e-6), 64, 96, 3
+    W = np.array(W, dtype=np.float64, order="C")
+    W = _plant_ties(W, 1, W.shape[0] // 8, 0)
+    W = _plant_ties(W, 2, W.shape[1] // 8, 1)
+    W = np.asfortranarray(W)
+    mult = synth.multiplier_abridged(9, W.shape[1], d, k, "arht")
+    P.lra.debug_counters(reset=True)
+    ora = O.cur_pipeline(W, mult, r, k, k, 3)
+    bufs, st = _run_gpu(P, h, W, mult, r, k, 3)
+    c = P.lra.debug_counters(reset=True)
+    assert st["status"] == 0
+    assert list(bufs.I.cpu().numpy()) == list(ora.I), "row pivots differ"
+    assert list(bufs.J.cpu().numpy()) == list(ora.J), "column pivots differ"
+    assert st["swaps"] == ora.ca.swaps and st["lu_steps"] == ora.ca.lu_steps
+    assert c["exact_rounds"] > 0, c
