@@ -1044,15 +1044,19 @@ def test_tie_rule_planted_ties_vs_oracle(P, tier):
     matrix, so that pivot candidates tie between warps, CTAs and cluster ranks.  Cluster tier:
     4096^2, k = 48 (16-CTA clusters); grid tier: 9000 x 600, k = 16 (18 cooperative CTAs);
     global tier: 3000 x 2600, k = 96.  Pivots, swap counts equal the oracle bit for bit, and the
-    exact second round ran (the fast per-unit decision was ambiguous at least once)."""
+    exact second round ran (the fast per-unit decision was ambiguous at least once).
+    W is i.i.d. Gaussian (well-conditioned generators): on a numerically rank-deficient W the
+    duplicate of a selected row has |c| = 1 + O(cond(G) eps), at the 1 + 1e-12 stop threshold,
+    and the oracle's own swap loop then cycles on rounding (reading C22: correct, not
+    reproducible), which is not what this test is about."""
     h = P.Handle(0)
     if tier == "cluster":
-        W, r, k, d = synth.factor_gaussian(31, 4096, 4096, 40, 1e-6), 32, 48, 4
+        shape, r, k, d = (4096, 4096), 32, 48, 4
     elif tier == "grid":
-        W, r, k, d = synth.factor_gaussian(32, 9000, 600, 12, 1e-6), 12, 16, 3
+        shape, r, k, d = (9000, 600), 12, 16, 3
     else:
-        W, r, k, d = synth.factor_gaussian(33, 3000, 2600, 80, 1e-6), 64, 96, 3
-    W = np.array(W, dtype=np.float64, order="C")
+        shape, r, k, d = (3000, 2600), 64, 96, 3
+    W = np.random.default_rng(30).standard_normal(shape)
     W = _plant_ties(W, 1, W.shape[0] // 8, 0)
     W = _plant_ties(W, 2, W.shape[1] // 8, 1)
     W = np.asfortranarray(W)
