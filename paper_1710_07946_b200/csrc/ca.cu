@@ -937,6 +937,7 @@ __global__ void __launch_bounds__(NT, 1) k_ca_ycplx(CAArgs a) {
 // (J <- maxvol(W[I,:]^T), cold in loop 0), 2L+2 = vertical step (I <- maxvol(W[:,J]), warm).
 template <int Q, int TPR, int NT, int OPK>
 __global__ void __launch_bounds__(NT, 1) k_ca(CAArgs a) {
+  if (a.skip && (a.skip[0] != 0 || a.skip[1] != 0)) return;   // row-sharded chain: step not needed
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ CAShared sh;
   Ctx c;

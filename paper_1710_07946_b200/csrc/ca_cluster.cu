@@ -384,6 +384,7 @@ __device__ __forceinline__ void mm_part(Kx<Q> &k, int q, double *out, const doub
 // (J <- maxvol(W[I,:]^T), cold in loop 0), 2L+2 = vertical step (I <- maxvol(W[:,J]), warm).
 template <int Q, int TPR, int OPK, bool QEQ = false>
 __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
+  if (a.skip && (a.skip[0] != 0 || a.skip[1] != 0)) return;   // row-sharded chain: step not needed
   constexpr int W = Q / TPR, QP = Q | 1;
   static_assert(W % 2 == 0 || W == 1, "W even");
   extern __shared__ __align__(16) unsigned char dsm[];

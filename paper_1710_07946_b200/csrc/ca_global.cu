@@ -295,6 +295,7 @@ __device__ __forceinline__ unsigned decide_exact(Sh<Q> &sh, unsigned mine, const
 
 template <int Q, int TPR, int OPK, bool QEQ = false>
 __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
+  if (a.skip && (a.skip[0] != 0 || a.skip[1] != 0)) return;   // row-sharded chain: step not needed
   constexpr int W = Q / TPR, RPP = NT / TPR;
   static_assert(W % 2 == 0, "W even");
   extern __shared__ __align__(16) double Xinv[];     // Q x Q

@@ -66,6 +66,8 @@ struct CAArgs {
   int32_t *yinfo;              // per problem x4: complex stage-2 result (scratch), or null
   int grid;                    // 1: grid tier (one problem over a cooperative grid)
   int y_warm;                  // 1: the maxvol on Y starts from the slots I0 (no LUP)
+  const int32_t *skip;         // row-sharded chain control (nullable): nothing is done when skip[0]
+                               // (an earlier step failed) or skip[1] (the C-A converged) is set
   void *gscratch;              // grid tier exchange buffers (ca_grid_scratch_bytes)
 };
 size_t ca_grid_scratch_bytes(int cs);
@@ -120,6 +122,17 @@ cudaError_t launch_scatter_wrows(const OpView &op, const int64_t *I, int q, int6
                                  cudaStream_t st);
 cudaError_t launch_scatter_g(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, int64_t row0,
                              double *dst, cudaStream_t st);
+// allgather assembly of the row-sharded blocks (shard.cu): local rows packed into a cm x q chunk
+// (zero rows beyond m_local), gathered chunks unpacked into the m_global x q block
+cudaError_t launch_pack_rows(const double *src, int64_t ld, int64_t m_local, int q, int64_t cm, double *chunk,
+                             cudaStream_t st);
+cudaError_t launch_pack_wcols(const OpView &op, const int64_t *J, int q, int64_t cm, double *chunk, cudaStream_t st);
+cudaError_t launch_unpack_chunks(const double *gathered, int64_t cm, int q, int nranks, int64_t m_global, double *dst,
+                                 cudaStream_t st);
+// device-side control of the row-sharded C-A chain (no host synchronization)
+cudaError_t launch_ctl_step(const lra_ca_stats *sts, int idx, int kind, int loop, int32_t *ctl, cudaStream_t st);
+cudaError_t launch_ctl_combine(const lra_ca_stats *sts, const int32_t *ctl, int has_y, lra_ca_stats *out,
+                               cudaStream_t st);
 cudaError_t launch_nucleus(const NucArgs &na, const FacArgs &fa, int64_t nb, cudaStream_t st, int *nlaunch, Prof *pf);
 
 struct ResArgs {

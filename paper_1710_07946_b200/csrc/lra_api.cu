@@ -24,6 +24,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
   const char *(*GetErrorString)(ncclResult_t);
 };
 static NcclApi &nccl() {
@@ -37,8 +38,10 @@ static NcclApi &nccl() {
     api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
     api.AllReduce = (decltype(api.AllReduce))dlsym(lib, "ncclAllReduce");
+    api.AllGather = (decltype(api.AllGather))dlsym(lib, "ncclAllGather");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather &&
+             api.GetErrorString;
   });
   return api;
 }
@@ -535,7 +538,7 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
 // cold (LUP) when start == nullptr, else warm from the slots `start`; slots -> out.
 static lra_status maxvol_block(lra_handle h, const double *blk, int64_t N, int q, const int64_t *start, int64_t *out,
                                double tol, double tau, int32_t cap, lra_ca_stats *st_dev, int32_t *status,
-                               int64_t *dummyJ, cudaStream_t st) {
+                               int64_t *dummyJ, cudaStream_t st, const int32_t *skip = nullptr) {
   CAArgs ca{};
   ca.op.kind = LRA_OP_DENSE;
   ca.op.dtype = LRA_F64;
@@ -558,6 +561,7 @@ static lra_status maxvol_block(lra_handle h, const double *blk, int64_t N, int q
   ca.J = dummyJ;
   ca.stats = st_dev;
   ca.status = status;
+  ca.skip = skip;
   cudaError_t e;
   const bool cluster = !ca_needs_global(N, q) && q <= 48 && N <= 16 * (q <= 24 ? 512 : 256);
   if (cluster) {
@@ -575,8 +579,18 @@ static lra_status maxvol_block(lra_handle h, const double *blk, int64_t N, int q
   return LRA_OK;
 }
 
-static size_t sharded_scratch(int64_t M, int64_t n, int64_t r, int64_t q, int32_t sweeps) {
+// The standard row split used by the allgather assembly: rank g holds rows [g cm, g cm + m_g),
+// cm = ceil(m / G).  Other splits are accepted and assembled by the owner-scatter + sum path.
+static bool standard_split(const lra_operand *W, int nranks, int rank, int64_t *cm_out) {
+  const int64_t M = W->m_global, cm = (M + nranks - 1) / nranks;
+  const int64_t r0 = (int64_t)rank * cm, ml = M - r0 < cm ? M - r0 : cm;
+  *cm_out = cm;
+  return W->row0 == r0 && W->m == ml;
+}
+
+static size_t sharded_scratch(int64_t M, int64_t n, int64_t r, int64_t q, int32_t sweeps, int nranks) {
   const int64_t Nmax = M > n ? M : n;
+  const int64_t cm = (M + nranks - 1) / nranks;
   Carve probe{nullptr, 0};
   probe.take<double>((size_t)Nmax * q);         // assembled block
   probe.take<double>((size_t)n * q);            // R^T for the final factor B
@@ -586,12 +600,23 @@ static size_t sharded_scratch(int64_t M, int64_t n, int64_t r, int64_t q, int32_
   probe.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
   probe.take<int32_t>(4);
   probe.take<int64_t>((size_t)q);               // dummy J output of standalone maxvol calls
+  probe.take<int32_t>(4);                       // chain control flags
+  probe.take<double>((size_t)cm * q);           // allgather: this rank's chunk
+  probe.take<double>((size_t)nranks * cm * q);  // allgather: all chunks
   return probe.off + 256;
 }
 
 static lra_status allreduce_sum(lra_handle h, double *buf, size_t count, cudaStream_t st) {
   if (h->nranks == 1 && !h->comm) return LRA_OK;
   NK(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, h->comm, st));
+  return LRA_OK;
+}
+static lra_status allgather(lra_handle h, const double *chunk, double *all, size_t count, cudaStream_t st) {
+  if (h->nranks == 1 && !h->comm) {
+    CK(cudaMemcpyAsync(all, chunk, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return LRA_OK;
+  }
+  NK(nccl().AllGather(chunk, all, count, ncclFloat64, h->comm, st));
   return LRA_OK;
 }
 
@@ -603,8 +628,11 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
   const int64_t M = W->m_global, n = W->n, q = k;
   const int64_t Nmax = M > n ? M : n;
   lra_status rs;
-  if ((rs = buf_reserve(&h->sh, &h->sh_bytes, sharded_scratch(M, n, r, k, sweeps), "the sharded blocks")) != LRA_OK)
+  if ((rs = buf_reserve(&h->sh, &h->sh_bytes, sharded_scratch(M, n, r, k, sweeps, h->nranks), "the sharded blocks")) !=
+      LRA_OK)
     return rs;
+  int64_t cm = 0;
+  const bool gather = standard_split(W, h->nranks, h->rank, &cm);
   Carve cv{(char *)h->sh, 0};
   double *blk = cv.take<double>((size_t)Nmax * q);
   double *Rt = cv.take<double>((size_t)n * q);
@@ -614,48 +642,68 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
   lra_ca_stats *sts = cv.take<lra_ca_stats>((size_t)(2 * sweeps + 1));
   int32_t *status = cv.take<int32_t>(4);
   int64_t *dJ = cv.take<int64_t>((size_t)q);
+  int32_t *ctl = cv.take<int32_t>(4);
+  double *chunk = cv.take<double>((size_t)cm * q);
+  double *chunks = cv.take<double>((size_t)h->nranks * cm * q);
   const OpView op = make_view(W);                 // local rows (op.m = m_local)
   lra_status s;
-  std::vector<lra_ca_stats> hs;
-  auto fetch = [&](int idx) -> lra_ca_stats {
-    lra_ca_stats x;
-    cudaMemcpyAsync(&x, sts + idx, sizeof(x), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    return x;
-  };
+  // The whole chain is stream-ordered: maxvol calls after a failure or after convergence do
+  // nothing (CAArgs::skip <- ctl), the early-exit rule and the statistics are evaluated on the
+  // device (k_ctl_step / k_ctl_combine), so the call never synchronizes the host and can be
+  // captured in a CUDA graph.  Every rank issues the same collectives in the same order.
   CK(cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st));
-  // stage 2: I <- maxvol(Y) on the assembled m_global x lbar sketch, or the given I0
-  int nst = 0;
-  if (Y) {
+  CK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int32_t), st));
+  CK(cudaMemsetAsync(sts, 0, (size_t)(2 * sweeps + 1) * sizeof(lra_ca_stats), st));
+  // blocks whose rows are the sharded rows: allgather of the packed local rows (standard
+  // split), else owner scatter + sum
+  auto assemble_rows = [&](bool from_y, const int64_t *Jc) -> lra_status {
+    lra_status s2;
+    if (gather) {
+      if (from_y) CK(launch_pack_rows((const double *)Y, ldy, W->m, (int)q, cm, chunk, st));
+      else CK(launch_pack_wcols(op, Jc, (int)q, cm, chunk, st));
+      if ((s2 = allgather(h, chunk, chunks, (size_t)cm * q, st)) != LRA_OK) return s2;
+      CK(launch_unpack_chunks(chunks, cm, (int)q, h->nranks, M, blk, st));
+      h->launches += 2;
+      return LRA_OK;
+    }
     CK(cudaMemsetAsync(blk, 0, (size_t)M * q * sizeof(double), st));
-    CK(launch_scatter_rows((const double *)Y, ldy, W->m, (int)q, W->row0, M, blk, st));
-    if ((s = allreduce_sum(h, blk, (size_t)M * q, st)) != LRA_OK) return s;
-    if ((s = maxvol_block(h, blk, M, (int)q, nullptr, I, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK) return s;
-    hs.push_back(fetch(nst++));
-    if (hs.back().status != LRA_OK) goto done;
+    if (from_y) CK(launch_scatter_rows((const double *)Y, ldy, W->m, (int)q, W->row0, M, blk, st));
+    else CK(launch_scatter_wcols(op, Jc, (int)q, W->row0, M, blk, st));
+    h->launches += 1;
+    return allreduce_sum(h, blk, (size_t)M * q, st);
+  };
+  int nst = 0;
+  // stage 2: I <- maxvol(Y) on the assembled m_global x lbar sketch, or the given I0
+  if (Y) {
+    if ((s = assemble_rows(true, nullptr)) != LRA_OK) return s;
+    if ((s = maxvol_block(h, blk, M, (int)q, nullptr, I, tol, tau, cap, sts + nst, status, dJ, st, ctl)) != LRA_OK)
+      return s;
+    CK(launch_ctl_step(sts, nst, 0, 0, ctl, st));
+    ++nst;
   } else {
     CK(cudaMemcpyAsync(I, I0, q * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   }
   for (int loop = 0; loop < sweeps; ++loop) {
-    // horizontal: J <- maxvol(W[I,:]^T) (cold in loop 0, else warm from J)
+    // horizontal: J <- maxvol(W[I,:]^T) (cold in loop 0, else warm from J); row I[s] is owned
+    // by one rank: owner scatter + sum
     CK(cudaMemsetAsync(blk, 0, (size_t)n * q * sizeof(double), st));
     CK(launch_scatter_wrows(op, I, (int)q, W->row0, blk, st));
     if ((s = allreduce_sum(h, blk, (size_t)n * q, st)) != LRA_OK) return s;
-    if ((s = maxvol_block(h, blk, n, (int)q, loop ? J : nullptr, J, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK)
+    if ((s = maxvol_block(h, blk, n, (int)q, loop ? J : nullptr, J, tol, tau, cap, sts + nst, status, dJ, st, ctl)) !=
+        LRA_OK)
       return s;
-    hs.push_back(fetch(nst++));
-    if (hs.back().status != LRA_OK) goto done;
+    CK(launch_ctl_step(sts, nst, 1, loop, ctl, st));
+    ++nst;
     // vertical: I <- maxvol(W[:,J]) warm from I
-    CK(cudaMemsetAsync(blk, 0, (size_t)M * q * sizeof(double), st));
-    CK(launch_scatter_wcols(op, J, (int)q, W->row0, M, blk, st));
-    if ((s = allreduce_sum(h, blk, (size_t)M * q, st)) != LRA_OK) return s;
-    if ((s = maxvol_block(h, blk, M, (int)q, I, I, tol, tau, cap, sts + nst, status, dJ, st)) != LRA_OK) return s;
-    hs.push_back(fetch(nst++));
-    if (hs.back().status != LRA_OK) goto done;
-    if (loop > 0 && hs[hs.size() - 1].swaps == 0 && hs[hs.size() - 2].swaps == 0) break;   // reading C13
+    if ((s = assemble_rows(false, J)) != LRA_OK) return s;
+    if ((s = maxvol_block(h, blk, M, (int)q, I, I, tol, tau, cap, sts + nst, status, dJ, st, ctl)) != LRA_OK) return s;
+    CK(launch_ctl_step(sts, nst, 2, loop, ctl, st));
+    ++nst;
+    h->launches += 4;
   }
   {
     // nucleus and factors: G = W[I,J] and R = W[I,:] assembled, the replicated Jacobi SVD
+    // (skipped on device when a step failed: the kernels read `status`)
     CK(cudaMemsetAsync(Rt, 0, (size_t)n * q * sizeof(double), st));
     CK(launch_scatter_wrows(op, I, (int)q, W->row0, Rt, st));
     if ((s = allreduce_sum(h, Rt, (size_t)n * q, st)) != LRA_OK) return s;
@@ -689,28 +737,11 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
     fa.Rt = Rt;
     int nl = 0;
     CK(launch_nucleus(na, fa, 1, st, &nl, &h->prof));
-    h->launches += nl;
+    h->launches += nl + 2;
   }
-done:
-  if (stats) {   // combine the per-call statistics as the fused kernel reports them
-    lra_ca_stats out{};
-    out.status = LRA_OK;
-    int sw_last_h = 0;
-    for (size_t i = 0; i < hs.size(); ++i) {
-      const lra_ca_stats &x = hs[i];
-      if (x.status != LRA_OK) out.status = x.status;
-      out.lu_steps += x.lu_steps;
-      out.swaps += x.swaps;
-      out.cap_hits += x.cap_hits;
-      const bool is_y = Y && i == 0;
-      const size_t j = Y ? i - 1 : i;           // 0 = h, 1 = v, ...
-      if (is_y) out.sketch_swaps = x.swaps;
-      else if (j % 2 == 0) { out.cert_cols = x.cert_rows; sw_last_h = x.swaps; }
-      else { out.cert_rows = x.cert_rows; out.loops_done += 1; }
-    }
-    (void)sw_last_h;
-    CK(cudaMemcpyAsync(stats, &out, sizeof(out), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
+  if (stats) {   // the per-call statistics combined on the device as the fused kernel reports them
+    CK(launch_ctl_combine(sts, ctl, Y ? 1 : 0, stats, st));
+    h->launches += 1;
   }
   return LRA_OK;
 }
@@ -1219,7 +1250,6 @@ lra_status lra_qrp_columns(lra_handle h, const lra_operand *W, const int64_t *I,
 // nb >= 1 sizes lra_batch over nb blocks shaped like W.  All four handle-owned buffers count.
 static lra_status workspace_sizes(lra_handle h, const lra_operand *W, int64_t r, int64_t k, int32_t sweeps,
                                   int64_t nb, size_t sz[4]) {
-  (void)h;
   lra_status s;
   if ((s = check_operand(W)) != LRA_OK) return s;
   if ((s = check_ca_shape(W, r, k, k, sweeps)) != LRA_OK) return s;
@@ -1237,7 +1267,7 @@ static lra_status workspace_sizes(lra_handle h, const lra_operand *W, int64_t r,
     }
     const size_t smp = (size_t)2 * 296 * sizeof(double2) + 256;
     ws = ws > smp ? ws : smp;
-    if (W->m_global > 0) sh = sharded_scratch(mg, n, r, k, sweeps);
+    if (W->m_global > 0) sh = sharded_scratch(mg, n, r, k, sweeps, h ? h->nranks : 1);
     if (ca_needs_global(maxN, (int)k) || W->m_global > 0) gm = ca_global_scratch_bytes(maxN, (int)k);
   } else {
     if (W->kind != LRA_OP_DENSE || W->m_global > 0) return fail(LRA_EINVAL, "lra_batch takes unsharded dense blocks");

@@ -1070,3 +1070,39 @@ def test_tie_rule_planted_ties_vs_oracle(P, tier):
     assert list(bufs.J.cpu().numpy()) == list(ora.J), "column pivots differ"
     assert st["swaps"] == ora.ca.swaps and st["lu_steps"] == ora.ca.lu_steps
     assert c["exact_rounds"] > 0, c
+
+
+def test_sharded_path_graph_capture_no_host_sync(P):
+    """The row-sharded chain (1-rank NCCL communicator, the allgather assembly, device-side
+    early exit and statistics) is stream-ordered with no host synchronization: after the
+    workspace reserve it captures into a CUDA graph (a host sync during capture would fail), the
+    replay reproduces the eager outputs bit for bit, and those equal the oracle (k = 16 ->
+    cluster tier; the chain stops early on a fixed point, so skipped steps are exercised)."""
+    from paper_1710_07946_b200 import pipeline
+    L = P.lra
+    h1 = P.Handle(0, nccl_id=P.nccl_unique_id(), nranks=1, rank=0)
+    W = synth.factor_gaussian(5, 1500, 1100, 30, 1e-10)
+    M = synth.multiplier_abridged(3, 1100, 2, 16, "arht")
+    Wd = L.Dense(L.to_colmajor(W), row0=0, m_global=1500)
+    Md = L.Multiplier(M)
+    L.lra_workspace_reserve(h1, Wd, 10, 16, 6)
+    bufs = pipeline.CurBuffers(1500, 1100, 10, 16)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pipeline.cur(h1, Wd, Md, 10, 16, 6, bufs=bufs)
+    torch.cuda.synchronize()
+    ora = O.cur_pipeline(W, M, 10, 16, 16, 6)
+    st = L.stats_to_numpy(bufs.stats)[0]
+    assert list(bufs.I.cpu().numpy()) == list(ora.I) and list(bufs.J.cpu().numpy()) == list(ora.J)
+    assert st["loops_done"] == ora.ca.loops_done and st["swaps"] == ora.ca.swaps
+    assert ora.ca.loops_done < 6                      # the early exit (reading C13) happened
+    eager = (bufs.I.clone(), bufs.J.clone(), bufs.U.clone(), bufs.num2.clone(), bufs.stats.clone())
+    for t in (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.stats):
+        t.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pipeline.cur(h1, Wd, Md, 10, 16, 6, bufs=bufs)
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.stats)):
+        assert torch.equal(a, b)

@@ -1,9 +1,15 @@
 """The row-sharded decomposition of the hot path, checked on CPU with
-world_size-2 gloo process groups against the single-process oracle.  Each rank holds rows
-[row0, row0 + m_local) of W; exactly as liblra.so's sharded path does with NCCL, every C-A
-block (the sketch Y, W[I,:]^T, W[:,J], W[I,J]) is assembled by an all-reduce SUM of
-owner-scattered rows into zeroed buffers (exact: x + 0 = x), the maxvol runs replicated, and
-the residual is the sum of the ranks' partial norms.  Test infrastructure only (uses oracle/)."""
+world_size-2 and -3 gloo process groups against the single-process oracle.  Each rank holds the
+rows [g cm, g cm + m_g) of W (cm = ceil(m / G), the standard split).  Exactly as liblra.so's
+sharded path does with NCCL:
+  * the blocks whose rows are W's rows (the sketch Y, W[:,J]) are assembled by an ALL-GATHER
+    of equal chunks (local rows packed, zero-padded to cm rows) and an unpack;
+  * the blocks with data-dependent ownership (W[I,:]^T, W[I,J]) by an all-reduce SUM of
+    owner-scattered rows into zeroed buffers (exact: x + 0 = x);
+  * the maxvol runs replicated; the early exit (reading C13) is decided from the replicated
+    swap counts (the library evaluates it on the device);
+  * the residual is the sum of the ranks' partial norms.
+Test infrastructure only (uses oracle/)."""
 import os
 import socket
 
@@ -31,18 +37,28 @@ def _sum(x):
     return t.numpy()
 
 
+def _gather_rows(local, cm, m, ws):
+    """local: (m_g, q) rows of this rank -> (m, q) assembled: every rank packs a cm x q chunk
+    (zero rows beyond m_g), all_gather, unpack rank g's chunk into rows g cm .. (k_pack_rows,
+    NCCL all-gather, k_unpack_chunks)."""
+    q = local.shape[1]
+    chunk = np.zeros((cm, q))
+    chunk[:local.shape[0]] = local
+    parts = [torch.zeros((cm, q), dtype=torch.float64) for _ in range(ws)]
+    dist.all_gather(parts, torch.from_numpy(chunk))
+    out = np.concatenate([p.numpy() for p in parts], axis=0)
+    return out[:m]
+
+
 def _worker(rank, ws, port, W, mult, r, k, sweeps, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     m, n = W.shape
-    bounds = np.linspace(0, m, ws + 1).astype(int)
-    row0, row1 = bounds[rank], bounds[rank + 1]
+    cm = -(-m // ws)
+    row0, row1 = rank * cm, min(m, (rank + 1) * cm)
     Wl = W[row0:row1]
-    # stage 1: local sketch rows (Y = W M is row-local) -> assembled Y
-    Yl = O.sketch(Wl, mult)
-    Y = np.zeros((m, k))
-    Y[row0:row1] = Yl
-    Y = _sum(Y)
+    # stage 1: local sketch rows (Y = W M is row-local) -> assembled Y (all-gather)
+    Y = _gather_rows(O.sketch(Wl, mult), cm, m, ws)
     I = O.maxvol(Y).S
     J = None
     steps = []
@@ -53,9 +69,7 @@ def _worker(rank, ws, port, W, mult, r, k, sweeps, out):
                 Rt[:, s] = Wl[i - row0]
         Rt = _sum(Rt)
         rh = O.maxvol(Rt, J)
-        Cb = np.zeros((m, k))
-        Cb[row0:row1] = Wl[:, rh.S]
-        Cb = _sum(Cb)
+        Cb = _gather_rows(Wl[:, rh.S], cm, m, ws)          # W[:,J] (all-gather)
         rv = O.maxvol(Cb, I)
         J, I = rh.S, rv.S
         steps += [rh.swaps, rv.swaps]
