@@ -23,6 +23,7 @@
 // layout with no padding beyond the next multiple of 16 rows / 32 columns.
 #include <cooperative_groups.h>
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -703,6 +704,495 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
   if (k.cs > 1) cluster_sync_all();   // keep every CTA's shared memory alive until done
 }
 
+
+// ============================================================================================
+// k_cacl2: the same method, schedule and arithmetic with TWO rows per row-group of threads —
+// slot A in registers (as k_cacl) and slot B in shared memory — so a CTA holds 2 NT / TPR
+// rows and a problem needs half the CTAs (config 2: 8-CTA clusters instead of 16: 15 problems
+// co-resident instead of 7).  The block B itself is no longer staged in shared memory: its
+// entries are read from global memory / L2 where needed (cold LUP start, G = B[S,:], and the
+// product C = B G^{-1}).  Every decision, update and tie rule is that of k_cacl, applied to
+// the union of both slots (slot A rows precede slot B rows in index order inside a CTA), so
+// the pivots are bit-identical.
+// --------------------------------------------------------------------------------------------
+
+// entry (row, col) of the current block: kind 0 = sketch Y, 1 = W[I,:]^T, 2 = W[:,J]
+template <int OPK>
+struct BSrc {
+  int kind;
+  const double *Y;
+  int64_t ldy;
+  OpView op;
+  const long long *I, *J;
+  __device__ __forceinline__ double operator()(int64_t row, int col) const {
+    if (kind == 0) return __ldg(Y + (int64_t)col * ldy + row);
+    if (kind == 1) return op_at<OPK>(op, I[col], row);
+    return op_at<OPK>(op, row, J[col]);
+  }
+};
+
+// Gauss-Jordan in place as gj_inplace, with G = B[S,:] read through the block source.
+template <int Q, class Src>
+__device__ __forceinline__ bool gj_src(Kx<Q> &k, const long long *S, int q, const Src &bsrc, double *Xo) {
+  constexpr int KR = (Q + 15) / 16, MC = (Q + 31) / 32;
+  Sh<Q> &sh = *k.sh;
+  double x[KR][MC];
+#pragma unroll
+  for (int a = 0; a < KR; ++a) {
+    const int r = k.warp + 16 * a;
+    const long long sr = r < q ? S[r] : 0;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const int col = k.lane + 32 * c;
+      x[a][c] = (r < q && col < q) ? bsrc(sr, col) : 0.0;
+    }
+  }
+  unsigned used = 0;
+  for (int s = 0; s < q; ++s) {
+    const int ls = s & 31, cs_ = s >> 5, sl = s & 1;
+    double v[KR];
+    unsigned long long key = 0ull;
+    int arow = 0x7fffffff;
+#pragma unroll
+    for (int a = 0; a < KR; ++a) {
+      double xv = x[a][0];
+#pragma unroll
+      for (int c = 1; c < MC; ++c) xv = (cs_ == c) ? x[a][c] : xv;
+      v[a] = __shfl_sync(0xffffffffu, xv, ls);
+      const int r = k.warp + 16 * a;
+      if (r < q && !((used >> a) & 1u)) {
+        const double av = fabs(v[a]);
+        const unsigned long long kk = (av != av) ? 0x7ff8000000000000ull : dkey(av);
+        if (arow == 0x7fffffff || kk > key) {
+          key = kk;
+          arow = r;
+        }
+      }
+    }
+    if (k.lane == 0) {
+      sh.gk[sl][k.warp] = key;
+      sh.gr[sl][k.warp] = arow;
+    }
+    __syncthreads();
+    const unsigned long long ck = k.lane < NW ? sh.gk[sl][k.lane] : 0ull;
+    const int cr = k.lane < NW ? sh.gr[sl][k.lane] : 0x7fffffff;
+    const unsigned long long mk = wmaxk(ck);
+    const int p = (int)__reduce_min_sync(0xffffffffu, (ck == mk && cr != 0x7fffffff) ? (unsigned)cr : 0xffffffffu);
+    if (p >= q) return false;
+    const int ap = p >> 4;
+    if (threadIdx.x == 0) sh.piv[s] = p;
+    if (k.warp == (p & 15)) {
+      double d = v[0];
+#pragma unroll
+      for (int a = 1; a < KR; ++a) d = (ap == a) ? v[a] : d;
+      const double rd = 1.0 / d;
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        const int col = k.lane + 32 * c;
+        double xv = x[0][c];
+#pragma unroll
+        for (int a = 1; a < KR; ++a) xv = (ap == a) ? x[a][c] : xv;
+        if (col < Q) sh.gp[col] = (col == s) ? rd : xv * rd;
+      }
+      if (k.lane == 0) sh.gd = d;
+    }
+    __syncthreads();
+    const double d = sh.gd;
+    if (!(fabs(d) > 0.0) || !isfinite(d)) return false;
+#pragma unroll
+    for (int a = 0; a < KR; ++a) {
+      const int r = k.warp + 16 * a;
+      const bool isp = (r == p);
+      if (isp) used |= 1u << a;
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        const int col = k.lane + 32 * c;
+        const double pv = col < Q ? sh.gp[col] : 0.0;
+        x[a][c] = isp ? pv : ((col == s) ? fma(-v[a], pv, 0.0) : fma(-v[a], pv, x[a][c]));
+      }
+    }
+  }
+  if (threadIdx.x < q) sh.pinv[sh.piv[threadIdx.x]] = threadIdx.x;
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < KR; ++a) {
+    const int r = k.warp + 16 * a;
+    if (r >= q) continue;
+    const int t = sh.pinv[r];
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const int col = k.lane + 32 * c;
+      if (col < q) Xo[t * Q + sh.piv[col]] = x[a][c];
+      else if (col < Q) Xo[t * Q + col] = 0.0;
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+template <int Q, int TPR, int OPK, bool QEQ = false>
+__global__ void __launch_bounds__(NT, 1) k_cacl2(CAArgs a) {
+  if (a.skip && (a.skip[0] != 0 || a.skip[1] != 0)) return;   // row-sharded chain: step not needed
+  constexpr int W = Q / TPR, RPH = NT / TPR;                  // RPH rows per slot per CTA
+  static_assert(W % 2 == 0 || W == 1, "W even");
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Sh<Q> sh;
+  double *SB = reinterpret_cast<double *>(dsm);               // slot B rows: SB[w * NT + tid]
+  double *Xp = SB + (size_t)W * NT;                           // 3 q x q parts (row stride Q)
+  Kx<Q> k;
+  k.sh = &sh;
+  k.cs = a.cs;
+  k.rank = a.cs > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  k.lane = threadIdx.x & 31;
+  k.warp = threadIdx.x >> 5;
+  k.par = 0;
+  k.tau = a.tau;
+  const double tol = a.tol;
+  const int q = QEQ ? Q : a.q;
+  const int64_t b = blockIdx.x / a.cs;
+  OpView op = a.op;
+  if (op.kind == LRA_OP_DENSE) op.w = (const char *)op.w + b * a.w_stride * (op.dtype == LRA_F32 ? 4 : 8);
+  const int tid = threadIdx.x;
+  const int ri = tid / TPR, sub = tid % TPR, jb = sub * W;
+  const int64_t r0 = (int64_t)k.rank * (2 * RPH);
+  const long long growA = r0 + ri, growB = r0 + RPH + ri;   // slot A rows precede slot B rows
+  int32_t status = LRA_OK;
+  int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0, sw_h = 0;
+  double cert_r = 0.0, cert_c = 0.0;
+  const bool yreal = a.Y != nullptr && !a.y_complex;
+  if (!yreal || a.y_warm) {
+    if (tid < q) sh.S[0][tid] = a.I0[b * a.i0_stride + tid];
+    if (a.yinfo) {
+      status = a.yinfo[4 * b + 0];
+      swaps = sk_swaps = a.yinfo[4 * b + 1];
+      caps = a.yinfo[4 * b + 2];
+      lu = a.yinfo[4 * b + 3];
+    }
+  }
+  if (tid < Q) sh.pm[tid] = 0.0;
+  for (int e = tid; e < 3 * Q * Q; e += NT) Xp[e] = 0.0;
+  __syncthreads();
+  const double *Yb = yreal ? reinterpret_cast<const double *>(a.Y) + b * a.y_stride : nullptr;
+  const int last = 2 * a.sweeps;
+  int ib = 0;
+  long long _tk = clock64();
+  for (int step = yreal ? 0 : 1; status == LRA_OK && step <= last; ++step) {
+    const int kind = step == 0 ? 0 : ((step & 1) ? 1 : 2);   // 0 = Y, 1 = h, 2 = v
+    const int64_t N = kind == 1 ? op.n : op.m;
+    long long *S = kind == 1 ? sh.S[1] : sh.S[0];
+    const bool fresh = step <= 1;
+    const bool cold = fresh && !(step == 0 && a.y_warm);
+    const bool carry = step >= 1 && step < last;
+    BSrc<OPK> bsrc{kind, Yb, a.ldy, op, sh.S[0], sh.S[1]};
+    const bool hasA = growA < N, hasB = growB < N;
+    // every CTA is done with the previous block's slots / rows before they change
+    if (k.cs > 1) cluster_sync_all(); else __syncthreads();
+    double row[W];
+    int myA = -1, myB = -1;
+    int nsw = 0;
+    bool ok = true;
+    double cert = 0.0;
+    bool cap_hit = false;
+    if (cold) {
+      // ---- Alg D.2 stage 1: LUP with the slack pivot rule over the rows of both slots
+      CC_T0();
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        row[w] = (hasA && jb + w < q) ? bsrc(growA, jb + w) : 0.0;
+        SB[w * NT + tid] = (hasB && jb + w < q) ? bsrc(growB, jb + w) : 0.0;
+      }
+      __syncthreads();
+      for (int t = 0; t < q && ok; ++t) {
+        const int st = t / W, wt = t - st * W;
+        double xA = rsel<W>(row, wt);
+        if (TPR > 1) xA = __shfl_sync(0xffffffffu, xA, (k.lane & ~(TPR - 1)) | st);
+        const double xB = SB[wt * NT + ri * TPR + st];
+        const double vA = (hasA && myA < 0) ? ((xA != xA) ? INFINITY : fabs(xA)) : -1.0;
+        const double vB = (hasB && myB < 0) ? ((xB != xB) ? INFINITY : fabs(xB)) : -1.0;
+        const double val = fmax(vA, vB);
+        auto first = [&](double thr) -> unsigned {
+          return vA >= thr ? (unsigned)growA : (unsigned)growB;
+        };
+        auto publish = [&](int p, unsigned cidx) {
+          if (hasA && (unsigned)growA == cidx) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) sh.pub[p][jb + w] = row[w];
+          } else if (hasB && (unsigned)growB == cidx) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) sh.pub[p][jb + w] = SB[w * NT + tid];
+          }
+        };
+        int p;
+        Dec d = pick(k, val, first, publish, p);
+        if (d.amb) d = pick_exact(k, val, d.M, first, publish, p);
+        if (!(d.M > 0.0) || !isfinite(d.M)) { ok = false; break; }
+        take_row(k, d, p, q, [&](int j, double xv) { sh.pm[j] = j > t ? xv : 0.0; });
+        const long long piv = d.idx;
+        if (threadIdx.x == 0) S[t] = piv;
+        if (hasA && growA == piv) myA = t;
+        if (hasB && growB == piv) myB = t;
+        if (hasA && myA < 0) {
+          const double f = xA / sh.prow[t];
+#pragma unroll
+          for (int w = 0; w < W; ++w) row[w] = rsub_mul(row[w], f, sh.pm[jb + w]);
+        }
+        if (hasB && myB < 0) {
+          const double f = xB / sh.prow[t];
+#pragma unroll
+          for (int w = 0; w < W; ++w) SB[w * NT + tid] = rsub_mul(SB[w * NT + tid], f, sh.pm[jb + w]);
+        }
+        __syncwarp();   // slot B columns are read across the row group (one warp) in the next step
+      }
+      __syncthreads();
+      CC_T1(1);
+      if (!ok) { status = LRA_ESINGULAR; break; }
+      lu += q;
+    } else {
+      for (int s2 = 0; s2 < q; ++s2) {
+        if (hasA && S[s2] == growA) myA = s2;
+        if (hasB && S[s2] == growB) myB = s2;
+      }
+    }
+    if (fresh) {
+      // ---- G = B[S,:] -> G^{-1} in part 0 (read through the block source)
+      ib = 0;
+      CC_T0();
+      ok = gj_src<Q>(k, S, q, bsrc, Xp);
+      CC_T1(3);
+      if (!ok) { status = LRA_ESINGULAR; break; }
+    } else {
+      // carried X0 = (G_prev^{-1})^T, one Newton step against the freshly gathered G
+      CC_T0();
+      const int cur = ib, pa = (ib + 1) % 3, pb = (ib + 2) % 3;
+      double *Xc = Xp + cur * Q * Q, *Xa = Xp + pa * Q * Q, *Xb = Xp + pb * Q * Q;
+      for (int e = tid; e < q * q; e += NT) {
+        const int r = e / q, c = e % q;
+        Xa[r * Q + c] = Xc[c * Q + r];
+      }
+      constexpr int KR = (Q + 15) / 16, MC = (Q + 31) / 32;
+#pragma unroll
+      for (int aa = 0; aa < KR; ++aa) {
+        const int r = k.warp + 16 * aa;
+        if (r >= q) continue;
+        const long long sr = S[r];
+#pragma unroll
+        for (int c = 0; c < MC; ++c) {
+          const int col = k.lane + 32 * c;
+          if (col < q) Xb[r * Q + col] = bsrc(sr, col);
+        }
+      }
+      __syncthreads();
+      mm_part<Q>(k, q, Xc, Xb, Xa, nullptr, -1.0);      // R  = I - G X0   -> cur
+      mm_part<Q>(k, q, Xb, Xa, Xc, Xa, 1.0);            // X1 = X0 + X0 R  -> pb
+      ib = pb;
+      CC_T1(2);
+    }
+    // ---- C = B G^{-1} for the rows outside S (both slots; B rows read from global / L2)
+    double rmxA = 0.0, rmxB = 0.0;
+    {
+      CC_T0();
+      const double *X = Xp + ib * Q * Q;
+      const bool doA = hasA && myA < 0, doB = hasB && myB < 0;
+      // Each thread loads the W entries B[row][jb..jb+W) of its half-row (all loads in flight
+      // together) into its own columns of SB; the row group then reads the whole row from SB
+      // (entry t lives with the thread of sub t / W).  Slot A first (accumulated in row[]), then
+      // slot B (accumulated in accB[], written back after the row group has read its B row).
+      auto load_half = [&](long long grow, bool live) {
+        double v[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) v[w] = (live && jb + w < q) ? bsrc(grow, jb + w) : 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) SB[w * NT + tid] = v[w];
+        __syncwarp();
+      };
+      auto product = [&](double (&acc)[W]) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[w] = 0.0;
+        for (int t = 0; t < q; ++t) {
+          const int st = t / W, wt = t - st * W;
+          const double bt = SB[wt * NT + ri * TPR + st];
+          if (W >= 2) {
+            const double2 *xr = reinterpret_cast<const double2 *>(X + t * Q + jb);
+#pragma unroll
+            for (int w = 0; w < W / 2; ++w) {
+              const double2 xv = xr[w];
+              acc[2 * w] = fma(bt, xv.x, acc[2 * w]);
+              acc[2 * w + 1] = fma(bt, xv.y, acc[2 * w + 1]);
+            }
+          } else {
+            acc[0] = fma(bt, X[t * Q + jb], acc[0]);
+          }
+        }
+      };
+      load_half(growA, doA);
+      product(row);
+      __syncwarp();
+      double accB[W];
+      load_half(growB, doB);
+      product(accB);
+      __syncwarp();
+      if (!doA) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) row[w] = 0.0;
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const double v = doB ? accB[w] : 0.0;
+        SB[w * NT + tid] = v;
+        rmxA = fmax(rmxA, fabs(row[w]));
+        rmxB = fmax(rmxB, fabs(v));
+      }
+      CC_T1(4);
+    }
+    __syncthreads();
+    // ---- Alg D.1 swap loop over the rows of both slots
+    {
+      CC_T0();
+      double *Xi = Xp + ib * Q * Q;
+      for (;;) {
+        const double cA = (hasA && myA < 0) ? rmxA : -1.0;
+        const double cB = (hasB && myB < 0) ? rmxB : -1.0;
+        const double mloc = fmax(cA, cB);
+        auto first = [&](double thr) -> unsigned {
+          unsigned res = 0xffffffffu;
+          if (cB >= thr) {
+#pragma unroll
+            for (int w = W - 1; w >= 0; --w)
+              if (jb + w < q && fabs(SB[w * NT + tid]) >= thr) res = (unsigned)(growB * q + jb + w);
+          }
+          if (cA >= thr) {
+#pragma unroll
+            for (int w = W - 1; w >= 0; --w)
+              if (jb + w < q && fabs(row[w]) >= thr) res = (unsigned)(growA * q + jb + w);
+          }
+          return res;
+        };
+        auto publish = [&](int p, unsigned cidx) {
+          if (cidx == 0xffffffffu) return;
+          const unsigned rr = cidx / (unsigned)q;
+          if (hasA && (unsigned)growA == rr) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) sh.pub[p][jb + w] = row[w];
+          } else if (hasB && (unsigned)growB == rr) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) sh.pub[p][jb + w] = SB[w * NT + tid];
+          }
+        };
+        int p;
+        Dec d = pick(k, mloc, first, publish, p);
+        if (!(d.M == d.M)) { ok = false; break; }
+        if (d.M <= 1.0 + tol || nsw >= a.cap) {
+          cert = fmax(d.M, 0.0);
+          cap_hit = d.M > 1.0 + tol;
+          break;
+        }
+        if (d.amb) d = pick_exact(k, mloc, d.M, first, publish, p);
+        const long long istar = d.idx / (unsigned)q;
+        const int jstar = (int)(d.idx % (unsigned)q);
+        take_row(k, d, p, q, [&](int j, double xv) {
+          sh.pm[j] = (j == jstar) ? xv - 1.0 : xv;
+          if (j == jstar) sh.rc = 1.0 / xv;
+        });
+        if (threadIdx.x == 0) S[jstar] = istar;
+        if (hasA && myA == jstar) {                    // leaves S: explicit row e_{j*}
+          myA = -1;
+#pragma unroll
+          for (int w = 0; w < W; ++w) row[w] = (jb + w == jstar) ? 1.0 : 0.0;
+        }
+        if (hasB && myB == jstar) {
+          myB = -1;
+#pragma unroll
+          for (int w = 0; w < W; ++w) SB[w * NT + tid] = (jb + w == jstar) ? 1.0 : 0.0;
+        }
+        if (hasA && growA == istar) myA = jstar;        // enters S
+        if (hasB && growB == istar) myB = jstar;
+        __syncwarp();
+        const int sj = jstar / W, wj = jstar - sj * W;
+        double xjA = rsel<W>(row, wj);
+        if (TPR > 1) xjA = __shfl_sync(0xffffffffu, xjA, (k.lane & ~(TPR - 1)) | sj);
+        const double xjB = SB[wj * NT + ri * TPR + sj];
+        const double rc = sh.rc;
+        __syncwarp();
+        rmxA = 0.0;
+        rmxB = 0.0;
+        if (hasA && myA < 0) {            // C <- C - C[:,j*] (C[i*,:] - e_j*) / c
+          const double g = xjA * rc;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            row[w] = fma(-g, sh.pm[jb + w], row[w]);
+            rmxA = fmax(rmxA, fabs(row[w]));
+          }
+        }
+        if (hasB && myB < 0) {
+          const double g = xjB * rc;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const double v = fma(-g, sh.pm[jb + w], SB[w * NT + tid]);
+            SB[w * NT + tid] = v;
+            rmxB = fmax(rmxB, fabs(v));
+          }
+        }
+        if (carry) {
+          constexpr int KR = (Q + 15) / 16, MC = (Q + 31) / 32;
+#pragma unroll
+          for (int aa = 0; aa < KR; ++aa) {
+            const int r = k.warp + 16 * aa;
+            if (r >= q) continue;
+            double *ir = Xi + r * Q;
+            const double gg = ir[jstar] * rc;
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < MC; ++c) {
+              const int col = k.lane + 32 * c;
+              if (col < q) ir[col] = fma(-gg, sh.pm[col], ir[col]);
+            }
+          }
+        }
+        ++nsw;
+      }
+      if (threadIdx.x == 0 && k.rank == 0) atomicAdd(&g_cc_cyc[7], (unsigned long long)(nsw + (cold ? q : 0)));
+      CC_T1(5);
+    }
+    if (!ok) { status = LRA_ESINGULAR; break; }
+    swaps += nsw;
+    caps += cap_hit;
+    if (kind == 0) {
+      sk_swaps = nsw;
+      cert_r = cert;
+    }
+    if (kind == 1) { cert_c = cert; sw_h = nsw; }
+    if (kind == 2) {
+      cert_r = cert;
+      ++loops;
+      if (step > 2 && sw_h == 0 && nsw == 0) break;           // fixed point (reading C13)
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && k.rank == 0) atomicAdd(&g_cc_cyc[6], (unsigned long long)(clock64() - _tk));
+  if (k.rank == 0) {
+    if (threadIdx.x < q) {
+      a.I[b * q + threadIdx.x] = sh.S[0][threadIdx.x];
+      a.J[b * q + threadIdx.x] = sh.S[1][threadIdx.x];
+    }
+    if (threadIdx.x == 0) {
+      a.status[b] = status;
+      if (a.stats) {
+        lra_ca_stats s;
+        s.status = status;
+        s.loops_done = loops;
+        s.lu_steps = lu;
+        s.swaps = swaps;
+        s.cap_hits = caps;
+        s.sketch_swaps = sk_swaps;
+        s.cert_rows = cert_r;
+        s.cert_cols = cert_c;
+        a.stats[b] = s;
+      }
+    }
+  }
+  if (k.cs > 1) cluster_sync_all();   // keep every CTA's shared memory alive until done
+}
+
 }  // namespace ccl
 
 static size_t cc_smem(int rpc, int Q) {
@@ -752,6 +1242,86 @@ static cudaError_t launch_cc_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   return e;
 }
 
+static size_t cc2_smem(int Q, int W) { return ((size_t)W * ccl::NT + (size_t)3 * Q * Q) * 8; }
+
+// two-slot kernel: 2 NT / TPR rows per CTA
+template <int Q, int TPR>
+static cudaError_t launch_cc2_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
+  constexpr int RPC2 = 2 * ccl::NT / TPR, W = Q / TPR;
+  int cs = 1;
+  while ((int64_t)cs * RPC2 < maxN) cs *= 2;
+  if (cs > 16) return cudaErrorInvalidConfiguration;
+  const size_t smem = cc2_smem(Q, W);
+  if (smem + sizeof(ccl::Sh<Q>) > 227 * 1024) return cudaErrorInvalidConfiguration;
+  a.cs = cs;
+  a.rpc = RPC2;
+  a.grid = 0;
+  if (cs_out) *cs_out = cs;
+  const bool qeq = a.q == Q;
+  void (*kern)(CAArgs) = a.op.kind == LRA_OP_FACTORED_CSR ? (qeq ? ccl::k_cacl2<Q, TPR, 2, true> : ccl::k_cacl2<Q, TPR, 2>)
+                         : (a.op.dtype == LRA_F64 ? (qeq ? ccl::k_cacl2<Q, TPR, 1, true> : ccl::k_cacl2<Q, TPR, 1>)
+                                                  : (qeq ? ccl::k_cacl2<Q, TPR, 0, true> : ccl::k_cacl2<Q, TPR, 0>));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nb * cs));
+  cfg.blockDim = dim3(ccl::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cs > 1 ? 1 : 0;
+  pf->begin("k_ca", st);
+  e = cudaLaunchKernelEx(&cfg, kern, a);
+  pf->end(st);
+  return e;
+}
+
+template <int Q, int TPR>
+static int cc2_active_t(int64_t maxN) {
+  constexpr int RPC2 = 2 * ccl::NT / TPR, W = Q / TPR;
+  int cs = 1;
+  while ((int64_t)cs * RPC2 < maxN) cs *= 2;
+  if (cs > 16) return 0;
+  const size_t smem = cc2_smem(Q, W);
+  void (*kern)(CAArgs) = ccl::k_cacl2<Q, TPR, 0>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(cs * 64));
+  cfg.blockDim = dim3(ccl::NT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// The two-slot kernel is used whenever the one-slot kernel would need a cluster of 2 or more.
+static bool use_two_slot(int64_t maxN, int q) {
+  static const int env = getenv("LRA_CA_SLOTS") ? atoi(getenv("LRA_CA_SLOTS")) : 2;   // diagnostics (A/B)
+  if (env == 1) return false;
+  const int rpc1 = q <= 24 ? ccl::NT : ccl::NT / 2;
+  return maxN > rpc1;
+}
+
 template <int Q, int TPR>
 static int cc_active_t(int64_t maxN) {
   constexpr int RPC = ccl::NT / TPR;
@@ -785,6 +1355,14 @@ static int cc_active_t(int64_t maxN) {
 // Problems of this shape the cluster tier runs concurrently (co-resident clusters; 0 if the
 // tier does not apply).  B200, config 2 (16-CTA clusters): 7.
 int ca_cluster_max_active(int64_t maxN, int q) {
+  if (use_two_slot(maxN, q)) {
+    if (q <= 8) return cc2_active_t<8, 1>(maxN);
+    if (q <= 16) return cc2_active_t<16, 1>(maxN);
+    if (q <= 24) return cc2_active_t<24, 1>(maxN);
+    if (q <= 32) return cc2_active_t<32, 2>(maxN);
+    if (q <= 48) return cc2_active_t<48, 2>(maxN);
+    return 0;
+  }
   if (q <= 8) return cc_active_t<8, 1>(maxN);
   if (q <= 16) return cc_active_t<16, 1>(maxN);
   if (q <= 24) return cc_active_t<24, 1>(maxN);
@@ -796,6 +1374,14 @@ int ca_cluster_max_active(int64_t maxN, int q) {
 // Cluster tier of the real C-A (q <= 48, at most 16 CTAs of NT / TPR rows): returns
 // cudaErrorInvalidConfiguration when the problem does not fit (caller falls back).
 cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf) {
+  if (use_two_slot(maxN, a.q)) {
+    if (a.q <= 8) return launch_cc2_t<8, 1>(a, nb, maxN, st, cs_out, pf);
+    if (a.q <= 16) return launch_cc2_t<16, 1>(a, nb, maxN, st, cs_out, pf);
+    if (a.q <= 24) return launch_cc2_t<24, 1>(a, nb, maxN, st, cs_out, pf);
+    if (a.q <= 32) return launch_cc2_t<32, 2>(a, nb, maxN, st, cs_out, pf);
+    if (a.q <= 48) return launch_cc2_t<48, 2>(a, nb, maxN, st, cs_out, pf);
+    return cudaErrorInvalidConfiguration;
+  }
   if (a.q <= 8) return launch_cc_t<8, 1>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 16) return launch_cc_t<16, 1>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 24) return launch_cc_t<24, 1>(a, nb, maxN, st, cs_out, pf);
