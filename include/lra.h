@@ -229,11 +229,22 @@ lra_status lra_leverage_scores(lra_handle h, const lra_operand *W, const int64_t
 /* Exactly(l) sampling and rescaling (Alg C.1 "algsmplex"; reading C31): l picks
    with Probability(i_t = i) = p_i driven by the caller's uniforms u (device, l values in
    [0, 1)): i_t = the smallest i with u_t P_{N-1} < P_i, P the sequential prefix sums of p.
+   p (device, N fp64) may be NULL: the uniform scores p_i = 1/N of the superfast variant of
+   Alg 9.1 (section slrasmpav).
    idx (device, l int64) gets the picks (with replacement), dscale (device, l fp64, may be
    NULL) the rescaling 1 / sqrt(l p_{i_t}).  status (device, may be NULL): nothing is done
    when it is not LRA_OK (chained after lra_leverage_scores). */
 lra_status lra_sample_exactly(lra_handle h, const double *p, int64_t N, int64_t l, const double *u, int64_t *idx,
                               double *dscale, const int32_t *status, void *stream);
+/* Expected(l) sampling and rescaling (Alg C.2 "algsmplexp"; reading C33): every i
+   in 0..N-1 is kept independently with probability pi_i = min{1, l p_i}, decided by the
+   caller's uniform u_i (device, N values in [0, 1)): kept iff u_i < pi_i (fp64).  The kept i,
+   in ascending order, go to idx (device, cap int64) and their rescaling 1 / min{1, sqrt(l p_i)}
+   to dscale (device, cap fp64, may be NULL); count (device int64) gets the number kept (its
+   expectation is sum_i pi_i <= l) — entries past cap are counted but not written.  p may be
+   NULL (uniform p_i = 1/N).  status as for lra_sample_exactly.  One CTA; asynchronous. */
+lra_status lra_sample_expected(lra_handle h, const double *p, int64_t N, int64_t l, const double *u, int64_t cap,
+                               int64_t *idx, double *dscale, int64_t *count, const int32_t *status, void *stream);
 
 /* maxvol of a dense fp64 block (Alg D.2 stage 1 + Alg D.1; readings C10-C12):
    B is N x q column-major (ld N, device, caller-owned, read only).  start == NULL: the LUP

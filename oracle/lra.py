@@ -412,6 +412,44 @@ def sample_exactly(p: np.ndarray, l: int, u: np.ndarray):
     return idx, 1.0 / np.sqrt(l * p[idx])
 
 
+def sample_expected(p: np.ndarray, l: int, u: np.ndarray):
+    """Alg C.2 (algsmplexp, "Expected(l)"), reading C33: ONE pass over j = 0..n-1
+    in ascending order; j is picked independently with probability π_j = min{1, l·p_j}, the
+    caller's uniform u_j ∈ [0, 1) deciding (picked iff u_j < π_j); the picked j, in ascending
+    order, are the sampled columns t = 0, 1, … (their number is random, expected Σ_j π_j ≤ l)
+    with the rescaling d_t = 1 / min{1, √(l·p_j)}."""
+    p = np.asarray(p, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    pi = np.minimum(1.0, l * p)
+    idx = np.nonzero(u < pi)[0].astype(np.int64)
+    return idx, 1.0 / np.minimum(1.0, np.sqrt(l * p[idx]))
+
+
+def cur_uniform(W, r: int, k: int, l: int, u_cols, u_rows, sampler: str = "exactly") -> "CurResult":
+    """Alg 9.1 (algcurlevsc) with UNIFORM leverage scores, the superfast variant of
+    §slrasmpav ("choosing the norms v_j^{(r)} equal to each other for all j",
+    so p_j = 1/n and p̄_i = 1/m): stage 2 samples the columns J with Alg C.1 (Exactly(l)) or
+    Alg C.2 (Expected(l)) from p_j = 1/n and the caller's uniforms u_cols; stages 3-4 sample the
+    rows I from p̄_i = 1/m (u_rows) — with uniform scores the scores of (C D)ᵀ are uniform too,
+    so no SVD is needed; stage 6: the constant rescalings D, D̄ cancel in D M⁺ D̄ and the
+    nucleus is the canonical U = W_{I,J,r}⁺ (reading C31).  Then CUR = A·B and ρ."""
+    W = np.asarray(W)
+    m, n = W.shape
+    op = DenseOperand(W)
+    pc = np.full(n, 1.0 / n)
+    pr = np.full(m, 1.0 / m)
+    if sampler == "exactly":
+        J, _ = sample_exactly(pc, l, u_cols)
+        I, _ = sample_exactly(pr, k, u_rows)
+    else:
+        J, _ = sample_expected(pc, l, u_cols)
+        I, _ = sample_expected(pr, k, u_rows)
+    U, Sr, sr, Tr = canonical_nucleus(op.block(I, J), r)
+    A, B = rank_r_factors(op.cols(J), op.rows(I), Sr, sr, Tr)
+    num2, den2 = cur_residual(W, A, B)
+    return CurResult(I, J, U, A, B, num2, den2, None, None)
+
+
 def cur_leverage(W, r: int, k: int, l: int, sweeps: int, I0, uniforms) -> "CurResult":
     """C-A iterations with the leverage-score sampling of DMM08 (stages 1–2 of Alg 9.1
     "algcurlevsc", with Alg C.1) as the subalgorithm of every horizontal and

@@ -174,6 +174,9 @@ cudaError_t launch_leverage_scores(const OpView &op, const int64_t *I, int k, in
                                    int32_t *status, void *scratch, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_sample_exactly(const double *p, int64_t N, int l, const double *u, double *P, int64_t *idx,
                                   double *dsc, const int32_t *status, cudaStream_t st, int *nlaunch, Prof *pf);
+cudaError_t launch_sample_expected(const double *p, int64_t N, int l, const double *u, int64_t cap, int64_t *idx,
+                                   double *dsc, int64_t *count, const int32_t *status, cudaStream_t st, int *nlaunch,
+                                   Prof *pf);
 cudaError_t launch_expand_columns(const OpView &op, const int64_t *I, int k, int64_t *J, int g0, int l, double tau,
                                   void *scratch, int *ok, cudaStream_t st, int *nlaunch, Prof *pf);
 cudaError_t launch_cert_norms(const OpView &op, const int64_t *I, const int64_t *J, int k, int l, const double *U,

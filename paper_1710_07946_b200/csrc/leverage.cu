@@ -7,7 +7,9 @@
 // a symmetric PSD G the SVD is the eigendecomposition: Sr = U_r, TS = U_r Lambda_r^{-1}), then
 // p_j = (1/r) sum_t (u_t . b_j)(u_t . b_j / lambda_t) = ||(V_r)_{j,:}||^2 / r, one thread per j.
 // Sampling: one CTA, the sequential prefix sum P (the oracle's order), then per draw the
-// smallest i with u P_{N-1} < P_i by binary search (reading C31).
+// smallest i with u P_{N-1} < P_i by binary search (reading C31); p == NULL means the uniform
+// scores p_j = 1/N of section slrasmpav.  Expected(l) (Alg C.2):
+// independent keep decisions u_j < min{1, l p_j} and an ordered compaction (reading C33).
 #include "kernels.cuh"
 
 namespace lra {
@@ -69,10 +71,11 @@ __global__ void __launch_bounds__(128) k_lev_scores(const double *B, int64_t N, 
 __global__ void __launch_bounds__(256) k_lev_sample(const double *p, int64_t N, int l, const double *u, double *P,
                                                     int64_t *idx, double *dsc, const int32_t *status) {
   if (status && *status != LRA_OK) return;
+  const double pu = 1.0 / (double)N;                  // p == NULL: uniform scores (section slrasmpav)
   if (threadIdx.x == 0) {
     double acc = 0.0;
     for (int64_t i = 0; i < N; ++i) {
-      acc = __dadd_rn(acc, p[i]);
+      acc = __dadd_rn(acc, p ? p[i] : pu);
       P[i] = acc;
     }
   }
@@ -87,8 +90,57 @@ __global__ void __launch_bounds__(256) k_lev_sample(const double *p, int64_t N, 
     }
     if (lo > N - 1) lo = N - 1;
     idx[t] = lo;
-    if (dsc) dsc[t] = 1.0 / sqrt((double)l * p[lo]);
+    if (dsc) dsc[t] = 1.0 / sqrt((double)l * (p ? p[lo] : pu));
   }
+}
+
+// Alg C.2 (Expected(l), reading C33): j is kept iff u_j < min{1, l p_j} (fp64, the oracle's
+// operations), the kept j compacted in ascending order by one CTA: per 1024-wide chunk a ballot
+// per warp, an exclusive scan of the 32 warp counts, then the running offset.  count gets the
+// number kept; idx / dsc receive the first min(count, cap) of them.
+__global__ void __launch_bounds__(1024) k_sample_expected(const double *p, int64_t N, int l, const double *u,
+                                                          int64_t cap, int64_t *idx, double *dsc, int64_t *count,
+                                                          const int32_t *status) {
+  if (status && *status != LRA_OK) return;
+  __shared__ int wc[32];
+  __shared__ int64_t base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double pu = 1.0 / (double)N;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < N; c0 += 1024) {
+    const int64_t j = c0 + threadIdx.x;
+    double pj = 0.0;
+    bool keep = false;
+    if (j < N) {
+      pj = p ? p[j] : pu;
+      keep = u[j] < fmin(1.0, __dmul_rn((double)l, pj));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wc[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      int v = wc[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wc[lane] = v;                                     // inclusive
+    }
+    __syncthreads();
+    const int64_t b0 = base;
+    if (keep) {
+      const int64_t t = b0 + (warp ? wc[warp - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+      if (t < cap) {
+        idx[t] = j;
+        if (dsc) dsc[t] = 1.0 / fmin(1.0, sqrt(__dmul_rn((double)l, pj)));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base = b0 + wc[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = base;
 }
 
 size_t leverage_scratch_bytes(int k, int r, int64_t N) {
@@ -139,6 +191,16 @@ cudaError_t launch_sample_exactly(const double *p, int64_t N, int l, const doubl
                                   double *dsc, const int32_t *status, cudaStream_t st, int *nlaunch, Prof *pf) {
   pf->begin("k_lev_sample", st);
   k_lev_sample<<<1, 256, 0, st>>>(p, N, l, u, P, idx, dsc, status);
+  pf->end(st);
+  *nlaunch += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_expected(const double *p, int64_t N, int l, const double *u, int64_t cap, int64_t *idx,
+                                   double *dsc, int64_t *count, const int32_t *status, cudaStream_t st, int *nlaunch,
+                                   Prof *pf) {
+  pf->begin("k_lev_sample", st);
+  k_sample_expected<<<1, 1024, 0, st>>>(p, N, l, u, cap, idx, dsc, count, status);
   pf->end(st);
   *nlaunch += 1;
   return cudaGetLastError();

@@ -1196,11 +1196,23 @@ lra_status lra_sample_exactly(lra_handle h, const double *p, int64_t N, int64_t 
                               double *dscale, const int32_t *status, void *stream) {
   lra_status st;
   if ((st = check_device(h)) != LRA_OK) return st;
-  if (!p || !u || !idx || N < 1 || l < 1) return fail(LRA_EINVAL, "need p, u, idx, N >= 1, l >= 1");
+  if (!u || !idx || N < 1 || l < 1 || l > INT32_MAX) return fail(LRA_EINVAL, "need u, idx, N >= 1, 1 <= l < 2^31");
   if ((st = ws_reserve(h, (size_t)N * 8 + 256)) != LRA_OK) return st;
   int nl = 0;
   CK(launch_sample_exactly(p, N, (int)l, u, (double *)h->ws, idx, dscale, status, (cudaStream_t)stream, &nl,
                            &h->prof));
+  h->launches += nl;
+  return LRA_OK;
+}
+
+lra_status lra_sample_expected(lra_handle h, const double *p, int64_t N, int64_t l, const double *u, int64_t cap,
+                               int64_t *idx, double *dscale, int64_t *count, const int32_t *status, void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if (!u || !count || N < 1 || l < 1 || l > INT32_MAX || cap < 0 || (cap > 0 && !idx))
+    return fail(LRA_EINVAL, "need u, count, N >= 1, 1 <= l < 2^31, cap >= 0 (idx when cap > 0)");
+  int nl = 0;
+  CK(launch_sample_expected(p, N, (int)l, u, cap, idx, dscale, count, status, (cudaStream_t)stream, &nl, &h->prof));
   h->launches += nl;
   return LRA_OK;
 }

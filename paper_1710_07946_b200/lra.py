@@ -92,6 +92,8 @@ def _load():
         lib.lra_leverage_scores.restype = C.c_int
         lib.lra_sample_exactly.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp, vp]
         lib.lra_sample_exactly.restype = C.c_int
+        lib.lra_sample_expected.argtypes = [vp, vp, i64, i64, vp, i64, vp, vp, vp, vp, vp]
+        lib.lra_sample_expected.restype = C.c_int
     if hasattr(lib, "lra_refine_columns"):
         lib.lra_contract_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i64, dbl, vp]
         lib.lra_contract_columns.restype = C.c_int
@@ -143,7 +145,7 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
             "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns", "lra_contract_columns",
-            "lra_refine_columns", "lra_leverage_scores", "lra_sample_exactly"]
+            "lra_refine_columns", "lra_leverage_scores", "lra_sample_exactly", "lra_sample_expected"]
 
 
 def debug_counters(reset=True):
@@ -375,10 +377,18 @@ def lra_leverage_scores(h, W, idx, side, r, p, status, stream=None):
                                      _ptr(status), _stream(stream)))
 
 
-def lra_sample_exactly(h, p, u, idx, dscale=None, status=None, stream=None):
-    """Alg C.1: idx (l,) int64 picks from p (N,) with the uniforms u (l,)."""
-    _check(lib().lra_sample_exactly(h.h, _ptr(p), p.numel(), idx.numel(), _ptr(u), _ptr(idx), _ptr(dscale),
+def lra_sample_exactly(h, p, u, idx, dscale=None, status=None, stream=None, N=None):
+    """Alg C.1: idx (l,) int64 picks from p (N,) with the uniforms u (l,); p None = uniform 1/N."""
+    N = p.numel() if p is not None else int(N)
+    _check(lib().lra_sample_exactly(h.h, _ptr(p), N, idx.numel(), _ptr(u), _ptr(idx), _ptr(dscale),
                                     _ptr(status), _stream(stream)))
+
+
+def lra_sample_expected(h, p, l, u, idx, count, dscale=None, status=None, stream=None):
+    """Alg C.2: keeps i iff u[i] < min(1, l p[i]) (u (N,)); the kept i in ascending order into idx
+    (cap = idx.numel()), their number into count ((1,) int64); p None = uniform 1/N."""
+    _check(lib().lra_sample_expected(h.h, _ptr(p), u.numel(), int(l), _ptr(u), idx.numel(), _ptr(idx), _ptr(dscale),
+                                     _ptr(count), _ptr(status), _stream(stream)))
 
 
 def lra_contract_columns(h, W, I, J, l, tie_slack=1e-12, stream=None):

@@ -175,3 +175,35 @@ def cur_leverage(h, W, r, k, l, sweeps, I0, uniforms, stream=None):
     den2 = torch.empty(1, dtype=torch.float64, device=dev)
     L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
     return I, J, U, A, B, num2, den2, status
+
+
+def cur_uniform(h, W, r, k, l, u_cols, u_rows, sampler="exactly", stream=None):
+    """Alg 9.1 with UNIFORM leverage scores (the superfast variant of section slrasmpav,
+    P:3363-3575; NEXT-4): the columns J from p_j = 1/n and the rows I from 1/m, sampled by
+    Alg C.1 (sampler "exactly": u_cols (l,), u_rows (k,)) or Alg C.2 ("expected": u_cols (n,),
+    u_rows (m,)), then the canonical nucleus / factors and the a-posteriori check.  With
+    "expected" the sample sizes are random: the counts are read back to size the nucleus call
+    (one host sync).  Returns (I, J, U, A, B, num2, den2, status (1,))."""
+    dev = u_cols.device
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if sampler == "exactly":
+        J = torch.empty(l, dtype=torch.int64, device=dev)
+        I = torch.empty(k, dtype=torch.int64, device=dev)
+        L.lra_sample_exactly(h, None, u_cols, J, stream=stream, N=W.n)
+        L.lra_sample_exactly(h, None, u_rows, I, stream=stream, N=W.m)
+    else:
+        J = torch.empty(W.n, dtype=torch.int64, device=dev)
+        I = torch.empty(W.m, dtype=torch.int64, device=dev)
+        cnt = torch.empty(2, dtype=torch.int64, device=dev)
+        L.lra_sample_expected(h, None, l, u_cols, J, cnt[0:1], stream=stream)
+        L.lra_sample_expected(h, None, k, u_rows, I, cnt[1:2], stream=stream)
+        lc, kc = (int(x) for x in cnt.cpu())
+        J, I = J[:lc].contiguous(), I[:kc].contiguous()
+    U = torch.empty((I.numel(), J.numel()), dtype=torch.float64, device=dev)
+    A = torch.empty((r, W.m), dtype=torch.float64, device=dev)
+    B = torch.empty((W.n, r), dtype=torch.float64, device=dev)
+    L.lra_nucleus_factors(h, W, I, J, r, U, A, B, status, stream=stream)
+    num2 = torch.empty(1, dtype=torch.float64, device=dev)
+    den2 = torch.empty(1, dtype=torch.float64, device=dev)
+    L.lra_cur_residual(h, W, A, B, r, num2, den2, stream=stream)
+    return I, J, U, A, B, num2, den2, status

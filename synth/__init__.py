@@ -265,3 +265,26 @@ def config5_torch(seed: int, m: int, n: int, row0: int = 0, rows: int = None, de
         z = torch.randn((n, block), generator=g, device=device, dtype=torch.float32)
         out[:, lo - row0:hi - row0] += noise_std * z[:, lo - b * block:hi - b * block]
     return out
+
+
+# ------------------------------------------------------------ NEXT-4: Table tb_Lp input
+def laplacian_tb_lp(n: int) -> np.ndarray:
+    """The discretized single-layer Laplacian of Table tb_Lp (after [HMT11, 7.1]):
+    w_ij = psi * int_{Gamma_1,j} log|2 omega^i - y| dy, Gamma_1 the unit circle, Gamma_1,j its
+    arc of angles [2 j pi / n, 2 (j+1) pi / n], omega = exp(2 pi sqrt(-1) / n) (the points
+    2 omega^i lie on Gamma_2 = C(0, 2)), psi such that ||W|| = 1 (spectral norm).
+    With phi = theta - 2 pi i / n, log|2 - e^{i phi}| = log 2 - sum_{k>=1} 2^-k cos(k phi) / k,
+    so the arc integral is (b - a) log 2 - sum_k 2^-k (sin(k b) - sin(k a)) / k^2 over the
+    shifted arc [a, b] (60 terms: below 2^-60).  W is circulant (w_ij depends on j - i mod n);
+    psi = 1 / max |eigenvalue| (the DFT of its first row).  fp64, deterministic (no seed)."""
+    a0 = 2.0 * np.pi * np.arange(n) / n                   # arc starts, i = 0
+    b0 = a0 + 2.0 * np.pi / n
+    kk = np.arange(1, 61, dtype=np.float64)
+    c = (b0 - a0) * np.log(2.0) - np.sum((0.5 ** kk)[None, :] * (np.sin(kk[None, :] * b0[:, None]) -
+                                                                 np.sin(kk[None, :] * a0[:, None])) / kk[None, :] ** 2,
+                                           axis=1)         # first row: i = 0, j = 0..n-1
+    W = np.empty((n, n))
+    for i in range(n):
+        W[i] = np.roll(c, i)                                # w_ij = c[(j - i) mod n]
+    psi = 1.0 / np.max(np.abs(np.fft.fft(c)))
+    return np.asfortranarray(W * psi)

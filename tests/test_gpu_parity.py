@@ -859,6 +859,109 @@ def test_sample_exactly_vs_oracle(P, h):
     assert np.allclose(d.cpu().numpy(), d_o, rtol=1e-15)
 
 
+@pytest.mark.parametrize("N", [1, 1023, 5000])
+def test_sample_expected_vs_oracle(P, h, N):
+    """Alg C.2 (Expected(l), reading C33) on scores with some l p_j > 1 (pi_j = 1), across
+    several 1024-wide compaction chunks and a ragged tail: the kept indices (ascending) and
+    their number are bit-exact, the rescalings equal to 1e-15."""
+    g = np.random.default_rng(63 + N)
+    p = g.random(N) ** 3
+    p /= p.sum()
+    l = max(1, N // 10)
+    u = g.random(N)
+    idx_o, d_o = O.sample_expected(p, l, u)
+    idx = torch.full((N,), -1, dtype=torch.int64, device="cuda")
+    d = torch.empty(N, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    P.lra.lra_sample_expected(h, torch.from_numpy(p).cuda(), l, torch.from_numpy(u).cuda(), idx, cnt, dscale=d)
+    torch.cuda.synchronize()
+    c = int(cnt.item())
+    assert c == len(idx_o)
+    assert list(idx.cpu().numpy()[:c]) == list(idx_o)
+    assert np.allclose(d.cpu().numpy()[:c], d_o, rtol=1e-15)
+    assert np.all(idx.cpu().numpy()[c:] == -1)
+
+
+def test_sample_expected_uniform_scores_and_cap(P, h):
+    """p = NULL (uniform scores 1/N): equal to the oracle on p = 1/N; with cap below the count,
+    the first cap kept indices are written and count still reports the full number."""
+    g = np.random.default_rng(64)
+    N, l = 4096, 300
+    u = g.random(N)
+    idx_o, d_o = O.sample_expected(np.full(N, 1.0 / N), l, u)
+    idx = torch.empty(N, dtype=torch.int64, device="cuda")
+    d = torch.empty(N, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    ut = torch.from_numpy(u).cuda()
+    P.lra.lra_sample_expected(h, None, l, ut, idx, cnt, dscale=d)
+    torch.cuda.synchronize()
+    c = int(cnt.item())
+    assert c == len(idx_o) and list(idx.cpu().numpy()[:c]) == list(idx_o)
+    assert np.allclose(d.cpu().numpy()[:c], d_o, rtol=1e-15)
+    cap = c // 2
+    small = torch.full((cap,), -1, dtype=torch.int64, device="cuda")
+    P.lra.lra_sample_expected(h, None, l, ut, small, cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == c and list(small.cpu().numpy()) == list(idx_o[:cap])
+
+
+def test_sample_exactly_uniform_scores(P, h):
+    """lra_sample_exactly with p = NULL equals the oracle on p = 1/N (sequential prefix sums
+    of the constant 1/N, then the inverse-CDF search)."""
+    g = np.random.default_rng(65)
+    N, l = 3000, 500
+    u = g.random(l)
+    idx_o, d_o = O.sample_exactly(np.full(N, 1.0 / N), l, u)
+    idx = torch.empty(l, dtype=torch.int64, device="cuda")
+    d = torch.empty(l, dtype=torch.float64, device="cuda")
+    P.lra.lra_sample_exactly(h, None, torch.from_numpy(u).cuda(), idx, dscale=d, N=N)
+    torch.cuda.synchronize()
+    assert list(idx.cpu().numpy()) == list(idx_o)
+    assert np.allclose(d.cpu().numpy(), d_o, rtol=1e-15)
+
+
+@pytest.mark.parametrize("case", ["rank6_exactly", "rank6_expected", "config2_exactly", "config2_expected"])
+def test_cur_uniform_vs_oracle(P, h, case):
+    """Alg 9.1 with uniform leverage scores (section slrasmpav): the sampled I, J equal the
+    oracle's (Alg C.1 or C.2 on p = 1/n, 1/m), U to 1e-8, rho to 1e-4 relative (1e-12
+    absolute on the exact-rank input, where W = CUR)."""
+    from paper_1710_07946_b200 import pipeline
+    g = np.random.default_rng(66)
+    if case.startswith("rank6"):
+        W = g.standard_normal((300, 6)) @ g.standard_normal((6, 260))
+        r, k, l = 6, 24, 24
+    else:
+        W = synth.config2(0)
+        r, k, l = 32, 48, 48
+    sampler = case.split("_")[1]
+    m, n = W.shape
+    uc, ur = (g.random(l), g.random(k)) if sampler == "exactly" else (g.random(n), g.random(m))
+    ora = O.cur_uniform(W, r, k, l, uc, ur, sampler=sampler)
+    I, J, U, A, B, num2, den2, st = pipeline.cur_uniform(h, _dense(P, W), r, k, l, torch.from_numpy(uc).cuda(),
+                                                         torch.from_numpy(ur).cuda(), sampler=sampler)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    assert list(I.cpu().numpy()) == list(ora.I) and list(J.cpu().numpy()) == list(ora.J)
+    assert np.allclose(U.cpu().numpy().T, ora.U, rtol=1e-8, atol=1e-8 * np.abs(ora.U).max())
+    rho = float(np.sqrt(num2.item() / den2.item()))
+    if case.startswith("rank6"):
+        assert rho <= 1e-12 and ora.rho <= 1e-12
+    else:
+        assert abs(rho / ora.rho - 1) <= 1e-4, (rho, ora.rho)
+
+
+@pytest.mark.parametrize("n,r", [(256, 31), (256, 39), (512, 35), (1024, 31)])
+def test_laplacian_tb_lp_qgauss20_vs_oracle(P, h, n, r):
+    """Table tb_Lp's input: the discretized single-layer Laplacian (fp64,
+    ||W|| = 1, singular values ~ 2^-f / f) pre-processed by 20 quasi-Gaussian bidiagonal
+    factors, k = l = r, 2 C-A sweeps: sketch, pivots, loops, swaps bit-exact, U to 1e-9,
+    rho within 1e-6 relative of the oracle's (~1e-6 .. 1e-7)."""
+    W = synth.laplacian_tb_lp(n)
+    M = synth.multiplier_qgauss(n, n, 20, r)
+    rho, ora = _check_pipeline(P, h, W, M, r, r, 2, rho_tol_rel=1e-6, y_exact=False)
+    assert rho < 1e-5
+
+
 @pytest.mark.parametrize("case", ["small", "config2"])
 def test_cur_leverage_vs_oracle(P, h, case):
     """Leverage-score C-A (DMM08's Alg 1 as the subalgorithm, Alg C.1 sampling with the same
