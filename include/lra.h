@@ -106,6 +106,15 @@ typedef struct {
   int32_t sketch_swaps;     /* swaps of the stage-2 maxvol on Y                              */
   double cert_rows;         /* max |C'| at exit of the last vertical step   (<= 1 + tol)     */
   double cert_cols;         /* max |C'| at exit of the last horizontal step (<= 1 + tol)     */
+  double logvol_final;      /* log v2(W[I,J]) = log|det W[I,J]| of the final generator (eq.
+                               eqvol; every swap multiplies it by |c*| > 1,
+                               P:6511-6513): the sum of log sigma_i of the nucleus' Jacobi SVD
+                               of the whole k x k generator; NaN if the nucleus did not run   */
+  double min_pivot_margin;  /* min over every pivot decision (cold LUP steps and swaps of all
+                               maxvol calls) of the top-2 margin (M - M2)/M, M2 the largest
+                               candidate other than the chosen one (reading C35): 0 = a tie
+                               broken by the index rule, tiny = a rounding-level reorder risk.
+                               Measured only with diagnostics on (lra_set_diagnostics), else NaN */
 } lra_ca_stats;
 
 /* Precision of the reconstruction A*B inside the full a-posteriori pass.
@@ -335,6 +344,13 @@ lra_status lra_debug_counters(uint64_t *out16 /* host */, int reset);
    waits for A, [6] epilogue warp 0 waits for accumulators, [7] epilogue warp 0 work,
    [8] tiles.  out16: host array of 16.  Synchronizes the device. */
 lra_status lra_debug_counters_residual(uint64_t *out16 /* host */, int reset);
+
+/* Diagnostics level of the handle (default 0).  level >= 1: lra_cross_approx and lra_batch
+   fill lra_ca_stats.min_pivot_margin; the C-A then runs on the global-memory tier (its pivots
+   are bit-identical to the on-chip tiers') with one extra grid reduction per pivot decision, so
+   it is a debugging mode, not a timed configuration.  ARFT (complex) sketches keep their tier
+   and report NaN.  EINVAL for level < 0. */
+lra_status lra_set_diagnostics(lra_handle h, int32_t level);
 
 /* Diagnostics (builds with -DLRA_CHECK_IDX=1 only; zeros otherwise): the first out-of-range
    data-dependent row / column index seen by a kernel: out4 (host) = { kernel id (1-2 nucleus

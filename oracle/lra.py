@@ -134,9 +134,24 @@ class MaxvolResult:
     lu_steps: int
     cap_hit: bool
     logdet: list = field(default_factory=list)   # log|det B[S,:]| after start and each swap
+    margins: list = field(default_factory=list)  # top-2 margin of every pivot decision (see pivot_margin)
 
 
-def lup_pivots(B: np.ndarray, tau: float = TAU) -> np.ndarray:
+def pivot_margin(cand: np.ndarray, chosen: int) -> float:
+    """Top-2 margin of one pivot decision (SURVEY §8(b) `min_pivot_margin`, reading C35):
+    (M − M₂)/M with M the largest candidate magnitude and M₂ the largest magnitude among the
+    candidates other than the chosen one (0 if there is none): 0 when the index rule broke a
+    tie inside the slack window (the chosen entry is not the unique maximum), small when a
+    rounding-level change could reorder the top two."""
+    a = np.asarray(cand, dtype=np.float64).copy()
+    M = float(a.max())
+    a[chosen] = -np.inf
+    M2 = float(a.max()) if len(a) > 1 else 0.0
+    M2 = max(M2, 0.0)
+    return (M - M2) / M
+
+
+def lup_pivots(B: np.ndarray, tau: float = TAU, margins=None) -> np.ndarray:
     """Cold start = Alg D.2 stage 1 on the tall block B (N×q): LU with
     partial (row) pivoting.  Step t: M_t = max over unchosen rows of |B'[i,t]|;
     p = smallest unchosen i with |B'[i,t]| ≥ (1−τ)·M_t (reading C11); then for every
@@ -152,6 +167,8 @@ def lup_pivots(B: np.ndarray, tau: float = TAU) -> np.ndarray:
         if not np.isfinite(M) or M <= 0.0:
             raise Singular(f"LUP: zero/non-finite pivot at step {t}")
         p = int(np.flatnonzero(a >= (1.0 - tau) * M)[0])
+        if margins is not None:
+            margins.append(pivot_margin(a[~chosen], int(np.sum(~chosen[:p]))))
         S[t] = p
         chosen[p] = True
         rest = ~chosen
@@ -169,8 +186,9 @@ def maxvol(B: np.ndarray, start=None, tau: float = TAU, tol: float = TOL, cap=No
     B = np.asarray(B)
     N, q = B.shape
     cap = 20 * q if cap is None else cap
+    margins = []
     if start is None:
-        S = lup_pivots(B, tau)
+        S = lup_pivots(B, tau, margins)
         lu_steps = q
     else:
         S = np.array(start, dtype=np.int64).copy()
@@ -190,8 +208,11 @@ def maxvol(B: np.ndarray, start=None, tau: float = TAU, tol: float = TOL, cap=No
         absC[S, :] = 0.0
         mstar = float(absC.max())
         if mstar <= 1.0 + tol or swaps >= cap:
-            return MaxvolResult(S, mstar, swaps, lu_steps, mstar > 1.0 + tol, logdet)
+            return MaxvolResult(S, mstar, swaps, lu_steps, mstar > 1.0 + tol, logdet, margins)
         flat = int(np.flatnonzero(absC.ravel() >= (1.0 - tau) * mstar)[0])
+        keep = np.ones(N, dtype=bool)
+        keep[S] = False                                  # candidates: the rows outside S
+        margins.append(pivot_margin(absC[keep, :].ravel(), int(np.sum(keep[:flat // q])) * q + flat % q))
         i, j = divmod(flat, q)
         S[j] = i
         swaps += 1
@@ -279,6 +300,16 @@ class CAResult:
     cert_cols: float
     logdet_steps: list      # log|det W[I,J]| after every C-A step (start of each maxvol)
     steps: list             # per-maxvol (side, swaps)
+    margins: list = field(default_factory=list)   # top-2 margins of every pivot decision
+
+    @property
+    def logvol_final(self) -> float:
+        """log v₂(W[I,J]) = log|det W[I,J]| of the final generator (eq. eqvol)."""
+        return self.logdet_steps[-1]
+
+    @property
+    def min_pivot_margin(self) -> float:
+        return min(self.margins) if self.margins else float("nan")
 
 
 def cross_approx(op, k: int, l: int, sweeps: int, Y=None, I0=None, J0=None,
@@ -297,10 +328,12 @@ def cross_approx(op, k: int, l: int, sweeps: int, Y=None, I0=None, J0=None,
         I = res.S
         lu, sw, ch = res.lu_steps, res.swaps, int(res.cap_hit)
         steps = [("sketch", res.swaps)]
+        margins = list(res.margins)
     else:
         I = np.array(I0, dtype=np.int64)
         lu = sw = ch = 0
         steps = []
+        margins = []
     J = None if J0 is None else np.array(J0, dtype=np.int64)
     logdet_steps = []
     cert_r = cert_c = float("nan")
@@ -314,11 +347,12 @@ def cross_approx(op, k: int, l: int, sweeps: int, Y=None, I0=None, J0=None,
         ch += int(rh.cap_hit) + int(rv.cap_hit)
         steps += [("h", rh.swaps), ("v", rv.swaps)]
         logdet_steps += rh.logdet + rv.logdet
+        margins += rh.margins + rv.margins
         J, I = rh.S, rv.S
         cert_c, cert_r = rh.cert, rv.cert
         if loop > 0 and rh.swaps == 0 and rv.swaps == 0:
             break
-    return CAResult(I, J, loops, lu, sw, ch, cert_r, cert_c, logdet_steps, steps)
+    return CAResult(I, J, loops, lu, sw, ch, cert_r, cert_c, logdet_steps, steps, margins)
 
 
 # ============================================ rectangular generators (Alg D.4, NEXT-3)

@@ -1018,6 +1018,8 @@ __global__ void __launch_bounds__(NT, 1) k_ca(CAArgs a) {
         s.sketch_swaps = sk_swaps;
         s.cert_rows = cert_r;
         s.cert_cols = cert_c;
+        s.logvol_final = __longlong_as_double(0x7ff8000000000000LL);   // filled by the nucleus
+        s.min_pivot_margin = __longlong_as_double(0x7ff8000000000000LL);
         a.stats[b] = s;
       }
     }

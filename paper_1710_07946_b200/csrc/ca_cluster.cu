@@ -697,6 +697,8 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
         s.sketch_swaps = sk_swaps;
         s.cert_rows = cert_r;
         s.cert_cols = cert_c;
+        s.logvol_final = __longlong_as_double(0x7ff8000000000000LL);   // filled by the nucleus
+        s.min_pivot_margin = __longlong_as_double(0x7ff8000000000000LL);
         a.stats[b] = s;
       }
     }
@@ -1186,6 +1188,8 @@ __global__ void __launch_bounds__(NT, 1) k_cacl2(CAArgs a) {
         s.sketch_swaps = sk_swaps;
         s.cert_rows = cert_r;
         s.cert_cols = cert_c;
+        s.logvol_final = __longlong_as_double(0x7ff8000000000000LL);   // filled by the nucleus
+        s.min_pivot_margin = __longlong_as_double(0x7ff8000000000000LL);
         a.stats[b] = s;
       }
     }

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
   int32_t status = LRA_OK;
   int lu = 0, swaps = 0, caps = 0, sk_swaps = 0, loops = 0, sw_h = 0;
   double cert_r = 0.0, cert_c = 0.0;
+  double mmin = 1.0;                     // diagnostics: min top-2 pivot margin (reading C35)
   const bool yreal = a.Y != nullptr && !a.y_complex;
   if (!yreal || a.y_warm) {
     if (tid < q) sh.S[0][tid] = a.I0[tid];
@@ -427,6 +428,19 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
           idx = decide_exact<Q>(sh, mine, g, par);
         }
         if (!(M > 0.0) || !isfinite(M)) { ok = false; break; }
+        if (a.diag) {    // top-2 margin: the largest candidate other than the chosen row
+          Cand c2;
+          c2.init();
+          for (int it = 0; it < iters; ++it) {
+            const int64_t row = r0 + (int64_t)it * RPP + tid / TPR;
+            if (row < r1 && sub == 0 && !g.inS[row] && (unsigned)row != idx) {
+              const double x = __ldcg(g.gC + (size_t)row * Q + t);
+              c2.add((x != x) ? INFINITY : fabs(x), (unsigned)row, tau);
+            }
+          }
+          decide<Q>(sh, c2, tau, g, par);
+          mmin = fmin(mmin, (M - fmax(sh.dM, 0.0)) / M);
+        }
         // winning row (its column-t.. values are current) -> prow, pm (masked j > t)
         if (tid < Q) {
           const double xv = tid < q ? __ldcg(g.gC + (size_t)idx * Q + tid) : 0.0;
@@ -540,6 +554,22 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
         }
         idx = decide_exact<Q>(sh, mine, g, par);
       }
+      if (a.diag) {      // top-2 margin over C' without the chosen entry
+        Cand c2;
+        c2.init();
+        for (int it = 0; it < iters; ++it) {
+          const int64_t row = r0 + (int64_t)it * RPP + tid / TPR;
+          if (row < r1 && !g.inS[row]) {
+            const double *src = g.gC + (size_t)row * Q + jb;
+            for (int w = 0; w < W; ++w) {
+              const unsigned li = (unsigned)(row * q + jb + w);
+              if (jb + w < q && li != idx) c2.add(fabs(__ldcg(src + w)), li, tau);
+            }
+          }
+        }
+        decide<Q>(sh, c2, tau, g, par);
+        mmin = fmin(mmin, (M - fmax(sh.dM, 0.0)) / M);
+      }
       istar = idx / (unsigned)q;
       jstar = (int)(idx % (unsigned)q);
       sold = S[jstar];
@@ -587,6 +617,8 @@ __global__ void __launch_bounds__(NT, 1) k_cagm(CAArgs a, GmArgs g) {
         s.sketch_swaps = sk_swaps;
         s.cert_rows = cert_r;
         s.cert_cols = cert_c;
+        s.logvol_final = __longlong_as_double(0x7ff8000000000000LL);   // filled by the nucleus
+        s.min_pivot_margin = a.diag ? mmin : __longlong_as_double(0x7ff8000000000000LL);
         a.stats[0] = s;
       }
     }

@@ -62,6 +62,7 @@ struct CAArgs {
   double tol, tau;
   int64_t *I, *J;              // outputs, stride q per problem
   lra_ca_stats *stats;         // per problem, may be null
+  int diag;                    // diagnostics (global tier only): min_pivot_margin
   int32_t *status;             // per problem
   int32_t *yinfo;              // per problem x4: complex stage-2 result (scratch), or null
   int grid;                    // 1: grid tier (one problem over a cooperative grid)
@@ -101,6 +102,7 @@ struct NucArgs {
   double *TS, *Sr;        // scratch: l x r and k x r per problem
   int32_t *status;        // per problem: already LRA_ESINGULAR -> skip
   const double *Gd;       // optional dense G = W[I,J] (k x l col-major) instead of gathering
+  lra_ca_stats *stats;    // optional, per problem: logvol_final (square generators)
 };
 struct FacArgs {
   OpView op;

@@ -92,6 +92,7 @@ struct lra_handle_s {
   size_t sh_bytes;
   void *qg;                       // quasi-Gaussian multiplier: built omega + integer work
   size_t qg_bytes;
+  int diag;                       // lra_set_diagnostics level
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -393,6 +394,12 @@ lra_status lra_debug_counters(uint64_t *out8, int reset) {
   return LRA_OK;
 }
 
+lra_status lra_set_diagnostics(lra_handle h, int32_t level) {
+  if (!h || level < 0) return fail(LRA_EINVAL, "need a handle and level >= 0");
+  h->diag = level;
+  return LRA_OK;
+}
+
 lra_status lra_debug_index_errors(int64_t *out4, int reset) {
   if (!out4) return fail(LRA_EINVAL, "null output");
   long long a[4], c[4];
@@ -480,6 +487,7 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   ca.status = status;
   ca.yinfo = y_complex ? yinfo : nullptr;
   ca.grid = 0;
+  ca.diag = (h->diag > 0 && !y_complex) ? 1 : 0;   // margins: measured on the global tier
   lra_status rs;
   if ((rs = buf_reserve(&h->gs, &h->gs_bytes, ca_grid_scratch_bytes(160), "the grid-tier exchange")) != LRA_OK)
     return rs;
@@ -487,7 +495,7 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   int cs = 0;
   const int64_t maxN = W->m > W->n ? W->m : W->n;
   cudaError_t e;
-  if (ca_needs_global(maxN, (int)k)) {
+  if (ca_needs_global(maxN, (int)k) || ca.diag) {
     if (y_complex) return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
     if ((rs = buf_reserve(&h->gm, &h->gm_bytes, ca_global_scratch_bytes(maxN, (int)k), "the global-memory C-A tier")) != LRA_OK)
       return rs;
@@ -512,6 +520,7 @@ static lra_status run_chain(lra_handle h, const lra_operand *W, int64_t w_stride
   na.TS = TS;
   na.Sr = Sr;
   na.status = status;
+  na.stats = stats;
   FacArgs fa{};
   fa.op = ca.op;
   fa.w_stride = w_stride;
@@ -701,6 +710,10 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
     ++nst;
     h->launches += 4;
   }
+  if (stats) {   // the per-call statistics combined on the device as the fused kernel reports them
+    CK(launch_ctl_combine(sts, ctl, Y ? 1 : 0, stats, st));
+    h->launches += 1;
+  }
   {
     // nucleus and factors: G = W[I,J] and R = W[I,:] assembled, the replicated Jacobi SVD
     // (skipped on device when a step failed: the kernels read `status`)
@@ -722,6 +735,7 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
     na.Sr = Sr;
     na.status = status;
     na.Gd = G;
+    na.stats = stats;
     FacArgs fa{};
     fa.op = op;
     fa.I = I;
@@ -738,10 +752,6 @@ static lra_status sharded_cross_approx(lra_handle h, const lra_operand *W, const
     int nl = 0;
     CK(launch_nucleus(na, fa, 1, st, &nl, &h->prof));
     h->launches += nl + 2;
-  }
-  if (stats) {   // the per-call statistics combined on the device as the fused kernel reports them
-    CK(launch_ctl_combine(sts, ctl, Y ? 1 : 0, stats, st));
-    h->launches += 1;
   }
   return LRA_OK;
 }
@@ -1087,7 +1097,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   const int64_t maxN = m > n ? m : n;
   if (cplx && ca_needs_global(maxN, (int)k))
     return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
-  const int act = ca_needs_global(maxN, (int)k) ? 0 : ca_cluster_max_active(maxN, (int)k);
+  const int act = (ca_needs_global(maxN, (int)k) || (h->diag > 0 && !cplx)) ? 0 : ca_cluster_max_active(maxN, (int)k);
   // While profiling (lra_profile_enable), the groups also run in order on one stream: every
   // kernel's event interval is then its own device time, not time spent queued behind
   // another group's kernels (the isolation pass of bench.py).

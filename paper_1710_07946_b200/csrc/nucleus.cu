@@ -218,6 +218,11 @@ __global__ void __launch_bounds__(512) k_nucleus(NucArgs a) {
       ord[y + 1] = v;
     }
     if (!(sig[ord[r - 1]] > 0.0) || !isfinite(sig[ord[0]])) a.status[b] = LRA_ESINGULAR;
+    if (a.stats && a.k == a.l) {   // log|det G| = sum of log sigma_i over the whole generator
+      double lv = 0.0;
+      for (int j = 0; j < l; ++j) lv += log(sig[j]);   // the l real columns (not the pad)
+      a.stats[b].logvol_final = lv;
+    }
   }
   __syncthreads();
   if (a.status[b] != LRA_OK) return;

@@ -91,6 +91,8 @@ __global__ void k_ctl_step(const lra_ca_stats *sts, int idx, int kind, int loop,
 __global__ void k_ctl_combine(const lra_ca_stats *sts, const int32_t *ctl, int has_y, lra_ca_stats *out) {
   lra_ca_stats o{};
   o.status = LRA_OK;
+  o.logvol_final = __longlong_as_double(0x7ff8000000000000LL);       // filled by the nucleus
+  o.min_pivot_margin = __longlong_as_double(0x7ff8000000000000LL);   // not measured here
   for (int i = 0; i < ctl[3]; ++i) {
     const lra_ca_stats &x = sts[i];
     if (x.status != LRA_OK) o.status = x.status;

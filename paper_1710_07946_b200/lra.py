@@ -45,8 +45,9 @@ class lra_multiplier(C.Structure):
 
 STATS_DTYPE = np.dtype([("status", np.int32), ("loops_done", np.int32), ("lu_steps", np.int32),
                         ("swaps", np.int32), ("cap_hits", np.int32), ("sketch_swaps", np.int32),
-                        ("cert_rows", np.float64), ("cert_cols", np.float64)])
-assert STATS_DTYPE.itemsize == 40
+                        ("cert_rows", np.float64), ("cert_cols", np.float64),
+                        ("logvol_final", np.float64), ("min_pivot_margin", np.float64)])
+assert STATS_DTYPE.itemsize == 56
 
 
 class LibraryMissing(RuntimeError):
@@ -121,6 +122,8 @@ def _load():
     lib.lra_debug_counters.restype = C.c_int
     lib.lra_debug_counters_residual.argtypes = [P(C.c_uint64), C.c_int]
     lib.lra_debug_counters_residual.restype = C.c_int
+    lib.lra_set_diagnostics.argtypes = [vp, i32]
+    lib.lra_set_diagnostics.restype = C.c_int
     lib.lra_debug_index_errors.argtypes = [P(i64), C.c_int]
     lib.lra_debug_index_errors.restype = C.c_int
     for f in ("lra_handle_create", "lra_preprocess", "lra_cross_approx", "lra_cur_residual", "lra_batch"):
@@ -140,7 +143,7 @@ def lib():
 
 EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cross_approx",
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
-            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_debug_index_errors",
+            "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_debug_index_errors", "lra_set_diagnostics",
             "lra_nccl_unique_id",
             "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
@@ -377,6 +380,11 @@ def lra_leverage_scores(h, W, idx, side, r, p, status, stream=None):
                                      _ptr(status), _stream(stream)))
 
 
+def lra_set_diagnostics(h, level):
+    """level >= 1: the C-A fills lra_ca_stats.min_pivot_margin (global tier; debugging mode)."""
+    _check(lib().lra_set_diagnostics(h.h, int(level)))
+
+
 def lra_sample_exactly(h, p, u, idx, dscale=None, status=None, stream=None, N=None):
     """Alg C.1: idx (l,) int64 picks from p (N,) with the uniforms u (l,); p None = uniform 1/N."""
     N = p.numel() if p is not None else int(N)
@@ -438,10 +446,10 @@ def lra_batch(h, nb, W, M, r, k, l, sweeps, I, J, U, num2, den2, stats=None, swa
 
 
 def stats_to_numpy(stats_t):
-    """Device stats buffer (uint8 tensor of 40·nb bytes) → numpy structured array."""
+    """Device stats buffer (uint8 tensor of 56·nb bytes) → numpy structured array."""
     return np.frombuffer(stats_t.cpu().numpy().tobytes(), dtype=STATS_DTYPE)
 
 
 def new_stats(nb=1, device="cuda"):
     import torch
-    return torch.zeros(40 * nb, dtype=torch.uint8, device=device)
+    return torch.zeros(STATS_DTYPE.itemsize * nb, dtype=torch.uint8, device=device)

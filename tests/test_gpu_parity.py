@@ -1209,3 +1209,65 @@ def test_sharded_path_graph_capture_no_host_sync(P):
     torch.cuda.synchronize()
     for a, b in zip(eager, (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.stats)):
         assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------ stats: logvol_final, min_pivot_margin
+@pytest.mark.parametrize("case", ["config1", "config2", "config2_gaussian"])
+def test_stats_logvol_final_vs_oracle(P, h, case):
+    """lra_ca_stats.logvol_final = log|det W[I,J]| of the final generator (the nucleus' Jacobi
+    singular values summed in log) equals the oracle's last logdet (slogdet of the LU) to 1e-10
+    relative; min_pivot_margin is NaN with diagnostics off."""
+    if case == "config1":
+        W, r, k, mult = synth.config1(0), 8, 8, synth.multiplier_abridged(0, 256, 3, 8, "arht")
+    else:
+        W, r, k = synth.config2(0), 32, 48
+        mult = synth.multiplier_abridged(0, 4096, 4, 48, "arht") if case == "config2" else \
+            synth.multiplier_gaussian(0, 4096, 48)
+    ora = O.cur_pipeline(W, mult, r, k, k, 3 if k == 48 else 2)
+    bufs, st = _run_gpu(P, h, W, mult, r, k, 3 if k == 48 else 2)
+    assert list(bufs.I.cpu().numpy()) == list(ora.I)
+    assert st["logvol_final"] == pytest.approx(ora.ca.logvol_final, rel=1e-10, abs=1e-10)
+    assert np.isnan(st["min_pivot_margin"])
+
+
+def test_stats_logvol_final_batch_vs_oracle(P, h):
+    """lra_batch on 16 config-3 blocks: every block's logvol_final equals the oracle's."""
+    from paper_1710_07946_b200 import pipeline
+    nb = 16
+    s, t = synth.cauchy_params(0, nb)
+    Wt = synth.cauchy_blocks_torch(s, t, "cuda")
+    M = synth.multiplier_abridged(0, 512, 3, 20, "arht")
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), P.lra.Multiplier(M), 16, 20, 2, nb)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)
+    for b in range(nb):
+        ora = O.cur_pipeline(synth.cauchy_block(s[b], t[b]), M, 16, 20, 20, 2)
+        assert st["logvol_final"][b] == pytest.approx(ora.ca.logvol_final, rel=1e-10, abs=1e-10), b
+
+
+@pytest.mark.parametrize("case", ["config1", "config2", "ties"])
+def test_stats_min_pivot_margin_diagnostics_vs_oracle(P, case):
+    """With diagnostics on (lra_set_diagnostics(h, 1)) the C-A runs on the global tier and
+    reports min_pivot_margin = min over every LUP step and swap of (M - M2)/M (reading C35):
+    equal to the oracle's to 1e-9 absolute, pivots unchanged; on planted exact ties the minimum
+    is exactly 0 on both sides (a tie broken by the index rule)."""
+    h = P.Handle(0)
+    P.lra.lra_set_diagnostics(h, 1)
+    if case == "config1":
+        W, r, k, mult, sw = synth.config1(0), 8, 8, synth.multiplier_abridged(0, 256, 3, 8, "arht"), 2
+    elif case == "config2":
+        W, r, k, mult, sw = synth.config2(0), 32, 48, synth.multiplier_abridged(0, 4096, 4, 48, "arht"), 3
+    else:
+        W = np.random.default_rng(30).standard_normal((3000, 2600))
+        W = _plant_ties(W, 1, 375, 0)
+        W = np.asfortranarray(_plant_ties(W, 2, 325, 1))
+        r, k, sw = 32, 48, 3
+        mult = synth.multiplier_abridged(9, 2600, 3, k, "arht")
+    ora = O.cur_pipeline(W, mult, r, k, k, sw)
+    bufs, st = _run_gpu(P, h, W, mult, r, k, sw)
+    assert list(bufs.I.cpu().numpy()) == list(ora.I) and list(bufs.J.cpu().numpy()) == list(ora.J)
+    assert st["swaps"] == ora.ca.swaps
+    assert abs(st["min_pivot_margin"] - ora.ca.min_pivot_margin) <= 1e-9, (st["min_pivot_margin"], ora.ca.min_pivot_margin)
+    if case == "ties":
+        assert ora.ca.min_pivot_margin == 0.0 and st["min_pivot_margin"] == 0.0
+    assert st["logvol_final"] == pytest.approx(ora.ca.logvol_final, rel=1e-10, abs=1e-10)

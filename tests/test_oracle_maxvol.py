@@ -280,3 +280,59 @@ def test_refine_columns_monotone_and_fixed_point():
     Jx = list(J) + [jstar]
     best_removal = max(range(len(Jx)), key=lambda t: vol(Jx[:t] + Jx[t + 1:]))
     assert Jx[best_removal] == jstar
+
+
+# ------------------------------------------- stats: top-2 pivot margins, final log-volume
+def test_pivot_margins_hand_examples():
+    """Top-2 margin (M − M₂)/M of each decision (reading C35), hand-evaluated:
+    LUP on (1, 1/2, 1/4)ᵀ: one step, M = 1, M₂ = 1/2 -> 1/2;  an exact tie (1, 1, .2)ᵀ -> 0;
+    a tie inside the slack window (1, 1 − 1e-13, .2)ᵀ: row 0 chosen, margin 1e-13;
+    maxvol of (4, 2, 1)ᵀ from S = [2]: C = (4, 2, 1), swap to row 0 with margin (4 − 2)/4,
+    then C = (1, 1/2, 1/4) is dominant — one margin, 1/2."""
+    r = lra.maxvol(np.array([[1.0], [0.5], [0.25]]))
+    assert r.margins == [0.5]
+    r = lra.maxvol(np.array([[1.0], [1.0], [0.2]]))
+    assert list(r.S) == [0] and r.margins == [0.0]
+    r = lra.maxvol(np.array([[1.0], [1.0 - 1e-13], [0.2]]))
+    assert list(r.S) == [0] and r.margins[0] == pytest.approx(1e-13, rel=1e-3)
+    r = lra.maxvol(np.array([[4.0], [2.0], [1.0]]), start=np.array([2]))
+    assert list(r.S) == [0] and r.swaps == 1 and r.margins == [0.5]
+
+
+def test_pivot_margin_two_columns_tie_across_columns():
+    """A swap decision over a 2-column C': the two largest entries in different columns and
+    rows, equal -> the smallest row-major index wins and the margin is 0."""
+    B = np.array([[1.0, 0.0], [0.0, 1.0], [3.0, 0.5], [0.5, 3.0]])
+    r = lra.maxvol(B, start=np.array([0, 1]))
+    assert r.margins[0] == 0.0 and list(r.S)[0] == 2
+
+
+def _det_bareiss(M):
+    """Exact integer determinant (fraction-free Bareiss elimination, Python ints)."""
+    A = [[int(x) for x in row] for row in M]
+    n = len(A)
+    sign, prev = 1, 1
+    for k in range(n - 1):
+        if A[k][k] == 0:
+            sw = next((i for i in range(k + 1, n) if A[i][k] != 0), None)
+            if sw is None:
+                return 0
+            A[k], A[sw] = A[sw], A[k]
+            sign = -sign
+        for i in range(k + 1, n):
+            for j in range(k + 1, n):
+                A[i][j] = (A[i][j] * A[k][k] - A[i][k] * A[k][j]) // prev
+        prev = A[k][k]
+    return sign * A[n - 1][n - 1]
+
+
+def test_logvol_final_equals_exact_integer_determinant():
+    """logvol_final = log|det W[I,J]| of the final generator (eq. eqvol with k = l): on an
+    integer-valued W it equals the log of the exact Bareiss determinant of W[I,J] to 1e-12."""
+    g = np.random.default_rng(12)
+    W = g.integers(-9, 10, (60, 50)).astype(np.float64)
+    ca = lra.cross_approx(lra.DenseOperand(W), 6, 6, 3, I0=np.arange(6))
+    d = _det_bareiss(W[np.ix_(ca.I, ca.J)])
+    assert d != 0
+    assert ca.logvol_final == pytest.approx(np.log(abs(float(d))), rel=1e-12)
+    assert 0.0 <= ca.min_pivot_margin <= 1.0 and len(ca.margins) == ca.lu_steps + ca.swaps
