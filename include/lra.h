@@ -293,6 +293,21 @@ lra_status lra_nucleus_factors(lra_handle h, const lra_operand *W, const int64_t
 lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A, const double *B, int64_t r,
                             const int64_t *rows, int64_t q, const int64_t *cols, int64_t s, double *stats3,
                             void *stream);
+
+/* Progressive-depth pre-processing ("typically at most three recursive steps";
+   NEXT-2): for d = 1, 2, ... the sketch with Ms[d-1] (the caller's multipliers of increasing
+   depth, realized host-side like any lra_multiplier; real kinds), the C-A (k = l, Y of m x k
+   fp64 caller-owned, tol / tie slack 1e-12, swap cap 20 k) with its nucleus and factors into
+   I, J, U, A, B, stats, then the superfast estimate est = sqrt(sum g^2 / sum W^2) over the
+   rows x cols sample (lra_error_sample, its 4 values left in stats4).  Stops at the first d
+   with est <= tol, or at d = nmult; *depth (host) = that d, *estimate (host) = its est, the
+   outputs hold that depth's CUR.  Synchronizes the stream once per depth (the stop decision). */
+lra_status lra_cur_progressive(lra_handle h, const lra_operand *W, const lra_multiplier *Ms, int32_t nmult, int64_t r,
+                               int64_t k, int32_t sweeps, double tol, const int64_t *rows, int64_t q,
+                               const int64_t *cols, int64_t s, void *Y, int64_t *I, int64_t *J, double *U, double *A,
+                               double *B, lra_ca_stats *stats, double *stats4, int32_t *depth, double *estimate,
+                               void *stream);
+
 /* A-priori error certificate of Corollary cowc1 (ii), eq. (eqnrm11), Frobenius
    norm: |W - CUR| <= delta ((|R| + |C| + delta + eta |C||R||U|) xi |U| + 1), C = W[:,J],
    R = W[I,:], U (l x k, device), eta = 1 if r = min(k,l) else 2, (1 - theta) xi = sqrt(k l),

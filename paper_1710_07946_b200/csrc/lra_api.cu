@@ -864,6 +864,38 @@ lra_status lra_error_sample(lra_handle h, const lra_operand *W, const double *A,
   return LRA_OK;
 }
 
+lra_status lra_cur_progressive(lra_handle h, const lra_operand *W, const lra_multiplier *Ms, int32_t nmult, int64_t r,
+                               int64_t k, int32_t sweeps, double tol, const int64_t *rows, int64_t q,
+                               const int64_t *cols, int64_t s, void *Y, int64_t *I, int64_t *J, double *U, double *A,
+                               double *B, lra_ca_stats *stats, double *stats4, int32_t *depth, double *estimate,
+                               void *stream) {
+  lra_status st;
+  if ((st = check_device(h)) != LRA_OK) return st;
+  if ((st = check_operand(W)) != LRA_OK) return st;
+  if (!Ms || nmult < 1 || !Y || !stats4 || !depth || !estimate) return fail(LRA_EINVAL, "bad arguments");
+  if (!(tol >= 0.0)) return fail(LRA_EINVAL, "tol >= 0");
+  cudaStream_t sm = (cudaStream_t)stream;
+  for (int32_t d = 1;; ++d) {
+    const lra_multiplier *M = &Ms[d - 1];
+    if (M->kind == LRA_MUL_ARFT) return fail(LRA_EUNSUPPORTED, "progressive depth runs real multipliers");
+    if ((st = lra_preprocess(h, W, M, Y, W->m, stream)) != LRA_OK) return st;
+    if ((st = lra_cross_approx(h, W, Y, W->m, 0, nullptr, r, k, k, sweeps, 1e-12, 1e-12, (int32_t)(20 * k), I, J, U,
+                               A, B, stats, stream)) != LRA_OK)
+      return st;
+    if ((st = lra_error_sample(h, W, A, B, r, rows, q, cols, s, stats4, stream)) != LRA_OK) return st;
+    double v[4];
+    CK(cudaMemcpyAsync(v, stats4, sizeof(v), cudaMemcpyDeviceToHost, sm));
+    CK(cudaStreamSynchronize(sm));
+    // the superfast estimate of rho (Section spstr): sqrt(sum g^2 / sum W^2) over the sample
+    const double est = v[3] > 0.0 ? sqrt(v[2] / v[3]) : INFINITY;
+    if (est <= tol || d >= nmult) {
+      *depth = d;
+      *estimate = est;
+      return LRA_OK;
+    }
+  }
+}
+
 lra_status lra_cur_certificate(lra_handle h, const lra_operand *W, const int64_t *I, const int64_t *J, const double *U,
                                int64_t k, int64_t l, int64_t r, double delta, double *out4, void *stream) {
   lra_status st;

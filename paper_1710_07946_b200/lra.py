@@ -80,6 +80,9 @@ def _load():
     lib.lra_preprocess_full.restype = C.c_int
     lib.lra_error_sample.argtypes = [vp, P(lra_operand), vp, vp, i64, vp, i64, vp, i64, vp, vp]
     lib.lra_error_sample.restype = C.c_int
+    lib.lra_cur_progressive.argtypes = [vp, P(lra_operand), P(lra_multiplier), i32, i64, i64, i32, dbl, vp, i64, vp,
+                                        i64, vp, vp, vp, vp, vp, vp, vp, vp, P(i32), P(dbl), vp]
+    lib.lra_cur_progressive.restype = C.c_int
     lib.lra_expand_columns.argtypes = [vp, P(lra_operand), vp, i64, vp, i64, i64, dbl, vp]
     lib.lra_expand_columns.restype = C.c_int
     lib.lra_nucleus_factors.argtypes = [vp, P(lra_operand), vp, vp, i64, i64, i64, vp, vp, vp, vp, vp]
@@ -145,7 +148,7 @@ EXPORTED = ["lra_handle_create", "lra_handle_destroy", "lra_preprocess", "lra_cr
             "lra_cur_residual", "lra_batch", "lra_last_error", "lra_launch_count", "lra_profile_enable",
             "lra_profile_read", "lra_debug_counters", "lra_debug_counters_residual", "lra_debug_index_errors", "lra_set_diagnostics",
             "lra_nccl_unique_id",
-            "lra_preprocess_full", "lra_error_sample", "lra_variance_bound",
+            "lra_preprocess_full", "lra_error_sample", "lra_cur_progressive", "lra_variance_bound",
             "lra_cur_certificate", "lra_expand_columns", "lra_nucleus_factors", "lra_workspace_query",
             "lra_workspace_reserve", "lra_maxvol", "lra_qrp_columns", "lra_contract_columns",
             "lra_refine_columns", "lra_leverage_scores", "lra_sample_exactly", "lra_sample_expected"]
@@ -423,6 +426,19 @@ def lra_cur_certificate(h, W, I, J, U, k, l, r, delta, stream=None):
     _check(lib().lra_cur_certificate(h.h, C.byref(W.struct()), _ptr(I), _ptr(J), _ptr(U), k, l, r, float(delta), out,
                                      _stream(stream)))
     return tuple(out)
+
+
+def lra_cur_progressive(h, W, Ms, r, k, sweeps, tol, rows, cols, Y, I, J, U, A, B, stats, stats4, stream=None):
+    """Progressive depth in the library: Ms = Multipliers of depth 1, 2, ... tried in order until
+    the sampled estimate is <= tol.  Returns (depth, estimate)."""
+    arr = (lra_multiplier * len(Ms))(*[M.struct() for M in Ms])
+    d = C.c_int32(0)
+    est = C.c_double(0.0)
+    _check(lib().lra_cur_progressive(h.h, C.byref(W.struct()), arr, len(Ms), r, k, sweeps, float(tol), _ptr(rows),
+                                     rows.numel(), _ptr(cols), cols.numel(), _ptr(Y), _ptr(I), _ptr(J), _ptr(U),
+                                     _ptr(A), _ptr(B), _ptr(stats), _ptr(stats4), C.byref(d), C.byref(est),
+                                     _stream(stream)))
+    return int(d.value), float(est.value)
 
 
 def lra_error_sample(h, W, A, B, r, rows, cols, stats3, stream=None):

@@ -76,25 +76,21 @@ def cur_preprocessed(h, W, M_full, r, k, sweeps, I0, stream=None):
 
 
 def cur_progressive(h, W, r, k, sweeps, tol, seed, rows, cols, dmax=6, stream=None):
-    """Progressive-depth pre-processing: d = 1, 2, 3, ... with the ARHT
-    multiplier of depth d (realized by the seeded generator) until the superfast sampled
-    estimate sqrt(sum g^2 / sum W^2) over rows x cols (lra_error_sample) is <= tol.
+    """Progressive-depth pre-processing through lra_cur_progressive: the ARHT
+    multipliers of depth d = 1 .. D (realized by the seeded generator; D = dmax or the largest
+    depth with 2^d | n) are handed to the library, which runs sketch -> C-A -> nucleus/factors ->
+    superfast sampled estimate per depth and stops at the first estimate <= tol.
     Returns (d, bufs, estimate)."""
     import synth
-    stats = torch.empty(4, dtype=torch.float64, device=W.Wt.device)
-    d = 1
-    while True:
-        M = L.Multiplier(synth.multiplier_abridged(seed, W.n, d, k, "arht"))
-        bufs = CurBuffers(W.m, W.n, r, k)
-        L.lra_preprocess(h, W, M, bufs.Y, stream=stream)
-        L.lra_cross_approx(h, W, bufs.Y, None, r, k, k, sweeps, bufs.I, bufs.J, bufs.U, bufs.A, bufs.B, bufs.stats,
-                           stream=stream)
-        L.lra_error_sample(h, W, bufs.A, bufs.B, r, rows, cols, stats, stream=stream)
-        _, _, ss, sw = stats.tolist()
-        est = (ss / sw) ** 0.5 if sw > 0 else float("inf")
-        if est <= tol or d >= dmax or W.n % (1 << (d + 1)):
-            return d, bufs, est
-        d += 1
+    D = 1
+    while D < dmax and W.n % (1 << (D + 1)) == 0:
+        D += 1
+    Ms = [L.Multiplier(synth.multiplier_abridged(seed, W.n, d, k, "arht")) for d in range(1, D + 1)]
+    bufs = CurBuffers(W.m, W.n, r, k)
+    stats4 = torch.empty(4, dtype=torch.float64, device=W.Wt.device)
+    d, est = L.lra_cur_progressive(h, W, Ms, r, k, sweeps, tol, rows, cols, bufs.Y, bufs.I, bufs.J, bufs.U, bufs.A,
+                                   bufs.B, bufs.stats, stats4, stream=stream)
+    return d, bufs, est
 
 
 def cur_rectangular(h, W, M, r, k, l, sweeps, stream=None):

@@ -506,16 +506,19 @@ def test_certificate_vs_oracle(P, h):
         assert a == pytest.approx(b, rel=1e-12) or (np.isinf(a) and np.isinf(b))
 
 
-def test_progressive_depth_vs_oracle(P, h):
-    """Progressive-depth mode: same accepted depth and pivots as the oracle."""
+@pytest.mark.parametrize("tol", [1e-3, 1e-30])
+def test_progressive_depth_vs_oracle(P, h, tol):
+    """Progressive-depth mode in the library (lra_cur_progressive): same accepted
+    depth, pivots and estimate as the oracle — accepted at once (tol 1e-3) or never (1e-30:
+    every depth 1..4 runs and the last one is returned)."""
     from paper_1710_07946_b200 import pipeline
     W = synth.factor_gaussian(3, 256, 256, 6, 1e-10)
     g = np.random.default_rng(0)
     rows, cols = g.choice(256, 40, replace=False), g.choice(256, 40, replace=False)
-    d_o, res_o, est_o = O.cur_progressive(W, 6, 8, 2, 1e-3, 1, rows, cols, dmax=4)
-    d, bufs, est = pipeline.cur_progressive(h, _dense(P, W), 6, 8, 2, 1e-3, 1, torch.from_numpy(rows).cuda(),
+    d_o, res_o, est_o = O.cur_progressive(W, 6, 8, 2, tol, 1, rows, cols, dmax=4)
+    d, bufs, est = pipeline.cur_progressive(h, _dense(P, W), 6, 8, 2, tol, 1, torch.from_numpy(rows).cuda(),
                                             torch.from_numpy(cols).cuda(), dmax=4)
-    assert d == d_o
+    assert d == d_o and d == (1 if tol > 1e-10 else 4)
     assert list(bufs.I.cpu().numpy()) == list(res_o.I) and list(bufs.J.cpu().numpy()) == list(res_o.J)
     assert est == pytest.approx(est_o, rel=1e-6)
 
