@@ -46,7 +46,13 @@ struct SketchArgs {
   void *y;
   int64_t y_stride;                 // batch stride of Y (elements of double / double2)
 };
-cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st, Prof *pf);
+cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, cudaStream_t st, Prof *pf,
+                          void *tc_scratch = nullptr, size_t tc_bytes = 0);
+// the Gaussian sketch on the tensor cores (sketch_tc.cu, reading C36)
+size_t sketch_tc_scratch_bytes(int64_t m, int64_t n, int64_t lbar, int64_t nb);
+size_t sketch_tc_zero_bytes();   // leading bytes of a fresh scratch buffer that must be zeroed once
+cudaError_t launch_sketch_tc(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo, void *scratch,
+                             size_t scratch_bytes, cudaStream_t st, Prof *pf);
 // NEXT-1: all n columns of W D H_{n,d} P (pinv: n ints of scratch)
 cudaError_t launch_transform_full(const SketchArgs &a, int *pinv, void *out, int64_t ldo, cudaStream_t st, Prof *pf);
 

@@ -93,6 +93,8 @@ struct lra_handle_s {
   void *qg;                       // quasi-Gaussian multiplier: built omega + integer work
   size_t qg_bytes;
   int diag;                       // lra_set_diagnostics level
+  void *sk;                       // tensor-core Gaussian sketch scratch (one slot per side stream)
+  size_t sk_bytes;
 };
 
 static lra_status ensure_streams(lra_handle h) {
@@ -261,6 +263,24 @@ static lra_status resolve_mult(lra_handle h, const lra_multiplier *M, int64_t n,
   return LRA_OK;
 }
 
+// Tensor-core Gaussian sketch (sketch_tc.cu, reading C36): scratch for nslots concurrent calls
+// of nb problems each; *per = 0 (SIMT kernel) for the other multiplier kinds or with
+// LRA_SKETCH_SIMT=1 (diagnostics: the order-preserving DFMA kernel, bit-identical to the oracle).
+static lra_status sketch_scratch(lra_handle h, const lra_multiplier *M, int64_t m, int64_t n, int64_t nb, int nslots,
+                                 size_t *per) {
+  static const bool simt = getenv("LRA_SKETCH_SIMT") != nullptr;
+  *per = 0;
+  if (M->kind != LRA_MUL_GAUSSIAN || simt) return LRA_OK;
+  const size_t b = (sketch_tc_scratch_bytes(m, n, M->lbar, nb) + 255) & ~(size_t)255;
+  lra_status s;
+  void *before = h->sk;
+  if ((s = buf_reserve(&h->sk, &h->sk_bytes, b * nslots, "the tensor-core sketch")) != LRA_OK) return s;
+  if (h->sk != before)   // fresh buffer: the split-tile accumulators / counters start at zero
+    for (int i = 0; i < nslots; ++i) CK(cudaMemset((char *)h->sk + i * b, 0, sketch_tc_zero_bytes()));
+  *per = b;
+  return LRA_OK;
+}
+
 // Reconstruction path of the full residual: fp32 W (or FAST) -> tensor-core
 // Ozaki kernel with S = 6 (PRECISE) / 3 (FAST) balanced base-256 digit slices; fp64 W in
 // PRECISE mode -> fp64 SIMT kernel.  LRA_RESID_SIMT=1 forces the SIMT kernel (diagnostics).
@@ -426,8 +446,10 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multipli
   lra_multiplier Mr;
   if ((s = resolve_mult(h, M, W->n, (cudaStream_t)stream, &Mr)) != LRA_OK) return s;
   SketchArgs a = make_sketch(W, &Mr, Y, ldy);
-  CK(launch_sketch(a, 1, Mr.omega, Mr.ld_omega, (cudaStream_t)stream, &h->prof));
-  h->launches += 1;
+  size_t per = 0;
+  if ((s = sketch_scratch(h, &Mr, W->m, W->n, 1, 1, &per)) != LRA_OK) return s;
+  CK(launch_sketch(a, 1, Mr.omega, Mr.ld_omega, (cudaStream_t)stream, &h->prof, per ? h->sk : nullptr, per));
+  h->launches += per ? 3 : 1;
   return LRA_OK;
 }
 
@@ -1147,6 +1169,17 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   lra_multiplier Mres;
   if ((s = resolve_mult(h, M0, n, st, &Mres)) != LRA_OK) return s;
   M0 = &Mres;
+  // A Gaussian sketch runs once for the whole batch on the tensor cores (one stream-K launch
+  // over every problem's tiles, before the fork); the other kinds are sketched per group.
+  size_t skper = 0;
+  if ((s = sketch_scratch(h, M0, m, n, nb, 1, &skper)) != LRA_OK) return s;
+  if (skper) {
+    SketchArgs sa = make_sketch(W0, M0, Y, m);
+    sa.w_stride = w_stride;
+    sa.y_stride = m * k;
+    CK(launch_sketch(sa, nb, M0->omega, M0->ld_omega, st, &h->prof, h->sk, skper));
+    h->launches += 3;
+  }
   CK(cudaEventRecord(h->fork, st));
   for (int i = 0; i < nside; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));
   // Every exit after the fork joins the side streams back into `stream` (so a captured graph
@@ -1178,8 +1211,10 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
     sa.w_stride = w_stride;
     sa.m_stride = m_stride;
     sa.y_stride = m * k;
-    CK(launch_sketch(sa, gn, Mg.omega, Mg.ld_omega, gs, &h->prof));
-    h->launches += 1;
+    if (!skper) {
+      CK(launch_sketch(sa, gn, Mg.omega, Mg.ld_omega, gs, &h->prof));
+      h->launches += 1;
+    }
     s = run_chain(h, &Wg, w_stride, Yg, m, m * k, cplx ? 1 : 0, nullptr, r, k, sweeps, swap_tol, tie_slack, swap_cap,
                   I + b0 * k, J + b0 * k, U ? U + b0 * k * k : nullptr, A + b0 * m * r, B + b0 * r * n, m * r, r * n,
                   stats ? stats + b0 : nullptr, status + b0, TS + b0 * k * r, Sr + b0 * k * r, yinfo + 4 * b0, gn, gs);

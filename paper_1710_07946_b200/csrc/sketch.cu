@@ -373,7 +373,11 @@ cudaError_t launch_transform_full(const SketchArgs &a, int *pinv, void *out, int
 }
 
 cudaError_t launch_sketch(const SketchArgs &a, int64_t nb, const double *omega, int64_t ldo,
-                          cudaStream_t st, Prof *pf) {
+                          cudaStream_t st, Prof *pf, void *tc_scratch, size_t tc_bytes) {
+  if (a.kind == LRA_MUL_GAUSSIAN && tc_scratch) {
+    const cudaError_t e = launch_sketch_tc(a, nb, omega, ldo, tc_scratch, tc_bytes, st, pf);
+    if (e != cudaErrorInvalidConfiguration) return e;   // W strides TMA cannot map: the SIMT kernel
+  }
   if (a.kind == LRA_MUL_GAUSSIAN) {
     pf->begin("k_sketch_gauss", st);
     const cudaError_t e = a.dtype == LRA_F32 ? launch_gauss<float>(a, nb, omega, ldo, st)
