@@ -94,7 +94,8 @@ def _spawn(args_in):
 
 
 class Clocks:
-    """nvidia-smi sampler (50 ms) for the clocks line of the JSON."""
+    """nvidia-smi sampler (10 ms) for the clocks line of the JSON; started before the warm-up and
+    awaited (ready) so that its first sample precedes the timed region."""
 
     def __init__(self, dev):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -103,10 +104,23 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "10"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
         self.t0 = self.t1 = None
+
+    def ready(self, timeout=10.0):
+        """Block until nvidia-smi has written its first sample (its start-up takes ~0.1-1 s)."""
+        if self.p is None:
+            return
+        t = time.time()
+        while time.time() - t < timeout:
+            try:
+                if os.path.getsize(self.f.name) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.01)
 
     def window(self, t0, t1):
         self.t0, self.t1 = t0, t1
@@ -132,7 +146,7 @@ class Clocks:
                 ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
                 ts = None
-            if self.t0 is None or ts is None or (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
+            if self.t0 is None or ts is None or (self.t0 - 0.01 <= ts <= self.t1 + 0.01):
                 rows.append(row)
         if not rows:
             rows = all_rows
@@ -337,6 +351,46 @@ def _isolated(h, fn, steps, ws):
 
 
 # ---------------------------------------------------------------- secondary workloads
+def run_sketch_tc(h, peaks, src, reps=20):
+    """The config-2 Gaussian sketch Y = W Omega (4096^2 fp32, lbar = 48) on the tensor cores
+    (sketch_tc.cu, reading C36): device time per call (events), per-kernel split (isolation), and
+    the tensor roofline of k_sketch_tc: int8 MACs issued (28 digit-slice products of M = 128,
+    N = 48, K = 32 per 128-row tile and K-step) over its launch time, against the int8 dense peak
+    = 2 x the measured bf16 peak (the guide's nominal ratio)."""
+    import torch
+    import synth
+    from paper_1710_07946_b200 import lra
+    W = torch.from_numpy(np.ascontiguousarray(synth.config2(0).T)).cuda()     # (n, m): column-major m x n
+    Wd = lra.Dense(W)
+    M = lra.Multiplier(synth.multiplier_gaussian(0, N_COLS, K))
+    Y = torch.empty((K, M_ROWS), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        lra.lra_preprocess(h, Wd, M, Y)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        lra.lra_preprocess(h, Wd, M, Y)
+    e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / reps * 1e3
+    prof, _ = _isolated(h, lambda i: lra.lra_preprocess(h, Wd, M, Y), reps, 1)
+    main_ms = prof.get("k_sketch_tc", (float("nan"), 1))[0]
+    tiles, ksteps = (M_ROWS + 127) // 128, (N_COLS + 31) // 32
+    macs = tiles * ksteps * 28 * 128 * 48 * 32
+    ach = 2.0 * macs / (main_ms * 1e-3) / 1e12
+    peak = 2.0 * peaks.get("bf16_tflops", 1590.0)
+    return {"workload": "cfg2 Gaussian sketch: W 4096x4096 fp32 (config 2) times Omega 4096x48 (fp32-rounded "
+                        "N(0,1)), Y fp64", "us_per_call": us,
+            "kernels_us": {k: v[0] * 1e3 for k, v in prof.items()},
+            "simt_reference_us": 208.0,
+            "roofline": {"kernel": "k_sketch_tc", "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s (int8)",
+                         "frac": ach / peak, "peak_source": src + " (2 x bf16)", "traffic": None,
+                         "ms_per_launch": main_ms},
+            "hbm_floor_us": M_ROWS * N_COLS * 4 / (peaks["hbm_gbs"] * 1e9) * 1e6}
+
+
 def run_cfg5(h, ws, rank, lrank, steps, warmup, peaks, src):
     """Config 5 at full size, row-sharded over the ws ranks (each generates its shard on device)."""
     import torch
@@ -486,6 +540,8 @@ def main():
         fn = run_cfg5 if args.workload == "cfg5" else run_cfg3
         a = (h, ws, rank, lrank) if args.workload == "cfg5" else (h, ws, rank)
         clocks = None if args.profile_only else Clocks(lrank)
+        if clocks:
+            clocks.ready()
         t0 = time.time()
         res = fn(*a, max(1, args.steps), args.warmup, peaks, peaks_src)
         if clocks:
@@ -516,6 +572,10 @@ def main():
     stats = lra.stats_to_numpy(bufs.stats)
     assert np.all(stats["status"] == 0), stats
     clocks = None if args.profile_only else Clocks(lrank)
+    if clocks:
+        clocks.ready()
+        step(0)                        # one more untimed step: the GPU back at load clocks after the wait
+        torch.cuda.synchronize()
     l0 = h.launches()
     t0 = time.time()
     ms = _timed(step, args.steps, ws, st)
@@ -632,6 +692,11 @@ def main():
     if not args.no_extra and not args.profile_only:
         del pools, Ws
         torch.cuda.empty_cache()
+        if rank == 0:
+            try:
+                extra["sketch_gaussian_tc"] = run_sketch_tc(h, peaks, peaks_src)
+            except Exception as ex:
+                extra["sketch_gaussian_tc"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
         for name, fn, a in (("cfg3", run_cfg3, (h, ws, rank)), ("cfg5", run_cfg5, (h, ws, rank, lrank))):
             try:
                 extra[name] = fn(*a, 5 if name == "cfg5" else 10, 2 if name == "cfg5" else 3, peaks, peaks_src)
