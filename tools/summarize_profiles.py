@@ -40,7 +40,7 @@ r = list(csv.reader(raw.splitlines()))
 h, u = r[0], r[1]
 idx = [h.index(w) for w in want if w in h]
 with open(os.path.join(out_dir, f"ncu_full_{tag}.txt"), "w") as f:
-    f.write("ncu --set full --clock-control none --import-source on (bench.py --profile-only --batch 14)\n")
+    f.write(f"ncu --set full --clock-control none --import-source on ({os.path.basename(rep)})\n")
     for row in r[2:]:
         f.write("; ".join(f"{h[i]}={row[i]} {u[i]}".strip() for i in idx) + "\n")
 print(open(os.path.join(out_dir, f"launches_{tag}.txt")).read()[:3000])
