@@ -500,7 +500,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=84)
+    ap.add_argument("--batch", type=int, default=90)
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "cfg3"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary workloads (cfg5, cfg3)")
