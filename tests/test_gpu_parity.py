@@ -3,6 +3,8 @@
 Tolerances (BASELINE.json): pivots (I, J in slot order) bit-exact; sketches
 bit-exact where both sides sum in the same order; fp64 mode |ρ_gpu − ρ_ora| ≤ 1e-12;
 fp32 mode |ρ_gpu/ρ_ora − 1| ≤ 1e-4; nucleus U to 1e-9 relative (different SVD codes)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -1361,3 +1363,54 @@ def test_sketch_simt_switch_keeps_bit_exact_sketch():
                           "torch.cuda.synchronize()\n"
                           "print('EXACT', np.array_equal(Y.cpu().numpy().T, O.sketch(W, M)))\n")
     assert "EXACT True" in out, out
+
+
+_CFG3 = {}
+
+
+def _cfg3_oracle_block(b):
+    from threadpoolctl import threadpool_limits
+    s, t, Ms = _CFG3["s"], _CFG3["t"], _CFG3["M"]
+    import scipy.linalg as sl
+    with threadpool_limits(1):          # one BLAS thread per worker process
+        W = synth.cauchy_block(s[b], t[b])
+        ora = O.cur_pipeline(W, dict(Ms, sp_row=Ms["sp_row"][b], sp_sign=Ms["sp_sign"][b]), 16, 20, 20, 2)
+        # the same CUR with the nucleus from LAPACK's other SVD driver (gesvd instead of numpy's
+        # gesdd): how far rho is determined at all when sigma_16 of the generator sits at the
+        # fp32 noise floor (reading C24)
+        Wd = np.asarray(W, np.float64)
+        Uu, Ss, Vt = sl.svd(Wd[np.ix_(ora.I, ora.J)], lapack_driver="gesvd")
+        Up = (Vt[:16].T / Ss[:16]) @ Uu[:, :16].T
+        rho_alt = np.linalg.norm(Wd - Wd[:, ora.J] @ Up @ Wd[ora.I, :]) / np.linalg.norm(Wd)
+    return list(ora.I), list(ora.J), ora.rho, float(rho_alt)
+
+
+def test_config3_all_4096_blocks_vs_oracle(P, h):
+    """BASELINE config 3 at full size (4096 Cauchy blocks, the bench's batch): every block's row
+    and column pivots equal the oracle's; rho within 1e-4 of the oracle's on all but <= 0.1 % of
+    the blocks, and on every block within the spread between two LAPACK SVD drivers for the
+    same nucleus (reading C24: the generators' sigma_16 sits at the fp32 noise floor with no gap
+    to sigma_17, and gesdd vs gesvd move rho by up to ~3e-3).  The oracle runs on all host cores."""
+    import multiprocessing as mp
+    from paper_1710_07946_b200 import pipeline
+    nb = 4096
+    s, t = synth.cauchy_params(0, nb)
+    Wt = synth.cauchy_blocks_torch(s, t, "cuda")
+    Ms = synth.multiplier_sparse_batch(0, nb, 512, 20)
+    bufs = pipeline.cur_batch(h, P.lra.Dense(Wt), P.lra.Multiplier(Ms), 16, 20, 2, nb)
+    torch.cuda.synchronize()
+    st = P.lra.stats_to_numpy(bufs.stats)
+    assert np.all(st["status"] == 0)
+    I, J = bufs.I.cpu().numpy(), bufs.J.cpu().numpy()
+    rho = np.sqrt(bufs.num2.cpu().numpy() / bufs.den2.cpu().numpy())
+    del Wt, bufs
+    _CFG3.update(s=s, t=t, M=Ms)        # inherited by the forked workers
+    with mp.get_context("fork").Pool(max(1, min(32, (os.cpu_count() or 2)))) as pool:
+        res = pool.map(_cfg3_oracle_block, range(nb), chunksize=16)
+    piv_bad = [b for b, (Io, Jo, _, _) in enumerate(res) if list(I[b]) != Io or list(J[b]) != Jo]
+    assert not piv_bad, (len(piv_bad), piv_bad[:10])
+    dev = np.array([abs(rho[b] / ro - 1) for b, (_, _, ro, _) in enumerate(res)])
+    spread = np.array([abs(ra / ro - 1) for (_, _, ro, ra) in res])
+    # every block within max(1e-4, the oracle's own driver spread); at most 0.1 % beyond 1e-4
+    assert np.all(dev <= np.maximum(1e-4, spread)), np.flatnonzero(dev > np.maximum(1e-4, spread))[:10]
+    assert np.sum(dev > 1e-4) <= nb // 1000, (np.flatnonzero(dev > 1e-4), np.median(spread))
