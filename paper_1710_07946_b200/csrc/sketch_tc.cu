@@ -53,6 +53,12 @@ __device__ unsigned long long g_stc_t[1024][4];   // STC_PROF: per CTA globaltim
 #define STC_PROF 0
 #endif
 #define STC_CLK() (STC_PROF ? clock64() : 0ll)
+#ifndef STC_NWS32
+#define STC_NWS32 8      // W stages for fp32 W
+#endif
+#ifndef STC_NBS
+#define STC_NBS 4        // Omega stages
+#endif
 #ifndef STC_SPIN
 #define STC_SPIN 1       // handshake waits without a suspend hint
 #endif
@@ -77,8 +83,8 @@ constexpr int NLEV = 7;           // kept levels L = s + u <= 6
 constexpr int NDW = 8;            // digitizer / epilogue warps
 constexpr int NMW = 3;            // MMA warps (12 warps in all: 168 registers per thread)
 constexpr int NTHR = 32 * (NDW + NMW + 1);
-constexpr int NBS = 4;            // Omega stages
-template <typename TW> constexpr int nws() { return sizeof(TW) == 4 ? 8 : 4; }   // W stages (TMA boxes 128 x 32)
+constexpr int NBS = STC_NBS;        // Omega stages
+template <typename TW> constexpr int nws() { return sizeof(TW) == 4 ? STC_NWS32 : 4; }   // W stages (TMA boxes 128 x 32)
 constexpr int SLOT = 2 * 48 * BM;  // int64 entries of one (hi, lo) tile buffer
 constexpr int KCHUNK = 256;       // max K-steps per accumulation (int32 safety)
 
