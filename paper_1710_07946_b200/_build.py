@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.environ.get("LRA_BUILD_OUT") or os.path.join(HERE, "liblra.so")   # LRA_BUILD_OUT: diagnostic builds
-SOURCES = ["lra_api.cu", "sketch.cu", "sketch_tc.cu", "ca.cu", "ca_cluster.cu", "ca_global.cu", "nucleus.cu", "residual.cu", "residual_tc.cu", "shard.cu", "expand.cu", "qrp.cu", "leverage.cu"]
+SOURCES = ["lra_api.cu", "sketch.cu", "sketch_tc.cu", "ca.cu", "ca_cluster.cu", "ca_global.cu", "ca_small.cu", "nucleus.cu", "residual.cu", "residual_tc.cu", "shard.cu", "expand.cu", "qrp.cu", "leverage.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"] + os.environ.get("LRA_EXTRA_FLAGS", "").split()

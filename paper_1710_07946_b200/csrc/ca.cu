@@ -1099,7 +1099,11 @@ static cudaError_t launch_ca_t(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t 
   CAArgs r = a;
   r.y_complex = 0;
   if (a.y_complex) r.Y = nullptr;
+  // small tier (ca_small.cu: one 128-thread CTA per problem, q <= 20, <= 512 rows), then the
   // cluster tier (ca_cluster.cu, q <= 48); k_ca's cluster form below covers 48 < q <= 64
+  e = launch_ca_small(r, nb, maxN, st, cs_out, pf);
+  if (e != cudaErrorInvalidConfiguration) return e;
+  cudaGetLastError();
   e = launch_ca_cluster(r, nb, maxN, st, cs_out, pf);
   if (e != cudaErrorInvalidConfiguration) return e;
   cudaGetLastError();

@@ -84,6 +84,10 @@ cudaError_t launch_ca(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *
 cudaError_t read_ca_counters(unsigned long long *out, bool reset);
 // cluster tier of the real C-A (ca_cluster.cu); cudaErrorInvalidConfiguration if it does not fit
 cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
+// small tier (ca_small.cu): one 128-thread CTA per problem, several problems per SM
+bool ca_small_fits(int64_t maxN, int q, int y_complex, int y_warm);
+int ca_small_max_active(int64_t maxN, int q);
+cudaError_t launch_ca_small(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t st, int *cs_out, Prof *pf);
 size_t nucleus_smem(int k, int l);
 bool nucleus_fits(int k, int l);
 cudaError_t read_nuc_counters(unsigned long long *out, bool reset);

@@ -1151,7 +1151,10 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
   const int64_t maxN = m > n ? m : n;
   if (cplx && ca_needs_global(maxN, (int)k))
     return fail(LRA_EUNSUPPORTED, "ARFT sketch with a block beyond the on-chip tiers");
-  const int act = (ca_needs_global(maxN, (int)k) || (h->diag > 0 && !cplx)) ? 0 : ca_cluster_max_active(maxN, (int)k);
+  const int act = (ca_needs_global(maxN, (int)k) || (h->diag > 0 && !cplx))
+                      ? 0
+                      : (ca_small_fits(maxN, (int)k, cplx ? 1 : 0, 0) ? ca_small_max_active(maxN, (int)k)
+                                                                       : ca_cluster_max_active(maxN, (int)k));
   // While profiling (lra_profile_enable), the groups also run in order on one stream: every
   // kernel's event interval is then its own device time, not time spent queued behind
   // another group's kernels (the isolation pass of bench.py).
