@@ -1414,3 +1414,35 @@ def test_config3_all_4096_blocks_vs_oracle(P, h):
     # every block within max(1e-4, the oracle's own driver spread); at most 0.1 % beyond 1e-4
     assert np.all(dev <= np.maximum(1e-4, spread)), np.flatnonzero(dev > np.maximum(1e-4, spread))[:10]
     assert np.sum(dev > 1e-4) <= nb // 1000, (np.flatnonzero(dev > 1e-4), np.median(spread))
+
+
+def test_small_tier_opt_in_matches_oracle():
+    """The opt-in small-block C-A tier (LRA_CA_SMALL=1, ca_small.cu; slower, kept for the
+    record) gives the oracle's pivots on a 96-block config-3 batch and on config 1 (subprocess:
+    the switch is read once per process)."""
+    out = _run_forced_env({"LRA_CA_SMALL": "1"},
+                          "import json, numpy as np, torch, synth\n"
+                          "from paper_1710_07946_b200 import Handle, lra, pipeline\n"
+                          "h = Handle(0); nb = 96\n"
+                          "s, t = synth.cauchy_params(0, nb)\n"
+                          "Wt = synth.cauchy_blocks_torch(s, t, 'cuda')\n"
+                          "Ms = synth.multiplier_sparse_batch(0, nb, 512, 20)\n"
+                          "h.profile(True)\n"
+                          "b = pipeline.cur_batch(h, lra.Dense(Wt), lra.Multiplier(Ms), 16, 20, 2, nb)\n"
+                          "torch.cuda.synchronize(); prof = h.profile_read(); h.profile(False)\n"
+                          "W1 = synth.config1(0); M1 = synth.multiplier_abridged(0, 256, 3, 8, 'arht')\n"
+                          "b1 = pipeline.cur(h, lra.Dense(lra.to_colmajor(W1)), lra.Multiplier(M1), 8, 8, 2)\n"
+                          "torch.cuda.synchronize()\n"
+                          "print(json.dumps({'I': b.I.cpu().tolist(), 'J': b.J.cpu().tolist(), 'k': sorted(prof),"
+                          " 'I1': b1.I.cpu().tolist(), 'J1': b1.J.cpu().tolist()}))\n")
+    import json
+    g = json.loads(out.strip().splitlines()[-1])
+    assert "k_ca_small" in g["k"], g["k"]
+    s, t = synth.cauchy_params(0, 96)
+    Ms = synth.multiplier_sparse_batch(0, 96, 512, 20)
+    for b in range(0, 96, 7):
+        ora = O.cur_pipeline(synth.cauchy_block(s[b], t[b]), dict(Ms, sp_row=Ms["sp_row"][b], sp_sign=Ms["sp_sign"][b]),
+                             16, 20, 20, 2, residual=False)
+        assert g["I"][b] == list(ora.I) and g["J"][b] == list(ora.J), b
+    ora1 = O.cur_pipeline(synth.config1(0), synth.multiplier_abridged(0, 256, 3, 8, "arht"), 8, 8, 8, 2)
+    assert g["I1"] == list(ora1.I) and g["J1"] == list(ora1.J)
