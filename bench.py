@@ -317,8 +317,10 @@ def _max_over_ranks(x, ws):
     return float(t.item())
 
 
-def _timed(fn, steps, ws, st):
-    """steps calls of fn bracketed by a barrier + synchronize, CUDA events on stream st; max over ranks."""
+def _timed(fn, steps, ws, st, streams=()):
+    """steps calls of fn bracketed by a barrier + synchronize, CUDA events on stream st (the other
+    streams fn launches on wait for the start event; the end event waits for all of them); max
+    over ranks."""
     import torch
     import torch.distributed as dist
     torch.cuda.synchronize()
@@ -328,8 +330,15 @@ def _timed(fn, steps, ws, st):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(st)
+    others = [s for s in streams if s != st]
+    for s in others:
+        s.wait_event(e0)
     for i in range(steps):
         fn(i)
+    for s in others:
+        ev = torch.cuda.Event()
+        ev.record(s)
+        st.wait_event(ev)
     e1.record(st)
     torch.cuda.synchronize()
     if ws > 1:
@@ -501,6 +510,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=90)
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
+                    help="batches in flight (2: consecutive steps alternate between two handles and streams)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "cfg3"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary workloads (cfg5, cfg3)")
@@ -562,27 +573,39 @@ def main():
     pools = [torch.from_numpy(hb).cuda() for hb in host]
     Ws = [lra.Dense(p) for p in pools]
     bufs = pipeline.BatchBuffers(B, R, K)
+    # Two batches in flight: consecutive steps alternate between two handles (each with its own
+    # side streams and scratch) on two streams, so one batch's tail (the last group's nucleus,
+    # factors and residual) overlaps the next batch's C-A waves.  The timed region spans both
+    # streams (they wait on the start event; the end event waits on both).
+    hs = [h, Handle(lrank)] if args.streams == 2 else [h]
+    sts = [torch.cuda.Stream() for _ in hs] if len(hs) > 1 else [st]
+    bufsx = [bufs] + [pipeline.BatchBuffers(B, R, K) for _ in hs[1:]]
 
     def step(i):
+        j = i % len(hs)
+        pipeline.cur_batch(hs[j], Ws[i % 2], M, R, K, SWEEPS, B, bufs=bufsx[j], stream=sts[j])
+
+    def step1(i):                      # one handle, the current stream (isolation pass)
         pipeline.cur_batch(h, Ws[i % 2], M, R, K, SWEEPS, B, bufs=bufs)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    stats = lra.stats_to_numpy(bufs.stats)
-    assert np.all(stats["status"] == 0), stats
+    for bx in bufsx:
+        stats = lra.stats_to_numpy(bx.stats)
+        assert np.all(stats["status"] == 0), stats
     clocks = None if args.profile_only else Clocks(lrank)
     if clocks:
         clocks.ready()
         step(0)                        # one more untimed step: the GPU back at load clocks after the wait
         torch.cuda.synchronize()
-    l0 = h.launches()
+    l0 = sum(x.launches() for x in hs)
     t0 = time.time()
-    ms = _timed(step, args.steps, ws, st)
+    ms = _timed(step, args.steps, ws, st, sts)
     t1 = time.time()
     if clocks:
         clocks.window(t0, t1)
-    launches = h.launches() - l0
+    launches = sum(x.launches() for x in hs) - l0
     clk = clocks.stop() if clocks else None
     total = ws * B * args.steps
     value = total / (ms / 1e3)
@@ -592,7 +615,7 @@ def main():
 
     # ---- isolation pass: the same two batches, kernels serialized, device time per kernel
     iso_steps = 2
-    prof, iso_ms = _isolated(h, step, iso_steps, ws)
+    prof, iso_ms = _isolated(h, step1, iso_steps, ws)
     kern_sum = sum(v[0] for v in prof.values())
     kernels = {k: {"ms_per_step": v[0], "launches_per_step": v[1], "share": v[0] / kern_sum}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
@@ -708,7 +731,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "batch_per_gpu": B, "l2": "inputs_gt_l2 (2 alternating batches of "
-                           f"{B} x 67 MB per GPU)", "parallelism": f"dp{ws} (independent matrices per rank)"},
+                           f"{B} x 67 MB per GPU)", "parallelism": f"dp{ws} (independent matrices per rank)",
+                           "batches_in_flight": len(hs)},
                 "roofline": roof, "stage_rooflines": stage,
                 "isolation": {"ms_per_step": iso_ms, "kernel_ms_sum": kern_sum, "steps": iso_steps,
                               "note": "same batches, lra_batch groups serialized on one stream, event pair per "
