@@ -449,7 +449,7 @@ lra_status lra_preprocess(lra_handle h, const lra_operand *W, const lra_multipli
   size_t per = 0;
   if ((s = sketch_scratch(h, &Mr, W->m, W->n, 1, 1, &per)) != LRA_OK) return s;
   CK(launch_sketch(a, 1, Mr.omega, Mr.ld_omega, (cudaStream_t)stream, &h->prof, per ? h->sk : nullptr, per));
-  h->launches += per ? 3 : 1;
+  h->launches += per ? 2 : 1;
   return LRA_OK;
 }
 
@@ -1181,7 +1181,7 @@ lra_status lra_batch(lra_handle h, int64_t nb, const lra_operand *W0, int64_t w_
     sa.w_stride = w_stride;
     sa.y_stride = m * k;
     CK(launch_sketch(sa, nb, M0->omega, M0->ld_omega, st, &h->prof, h->sk, skper));
-    h->launches += 3;
+    h->launches += 2;
   }
   CK(cudaEventRecord(h->fork, st));
   for (int i = 0; i < nside; ++i) CK(cudaStreamWaitEvent(h->side[i], h->fork, 0));

@@ -184,13 +184,13 @@ __device__ __forceinline__ unsigned long long absbits(TW v) {
   return (unsigned long long)__double_as_longlong(fabs((double)v));
 }
 template <typename TW>
-__global__ void __launch_bounds__(256) k_stc_rowmax(const TW *W, int64_t ldw, int64_t w_stride, int64_t m, int64_t n,
-                                                    int64_t cols_per, unsigned long long *rowmax) {
-  const int64_t b = blockIdx.z;
-  const int64_t i0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+__device__ __forceinline__ void stc_rowmax(const TW *W, int64_t ldw, int64_t w_stride, int64_t m, int64_t n,
+                                           int64_t cols_per, unsigned long long *rowmax, int64_t bx, int64_t by,
+                                           int64_t b) {
+  const int64_t i0 = (bx * 256 + threadIdx.x) * 4;
   if (i0 >= m) return;
   const TW *p = W + b * w_stride + i0;
-  const int64_t j0 = (int64_t)blockIdx.y * cols_per, j1 = min(n, j0 + cols_per);
+  const int64_t j0 = by * cols_per, j1 = min(n, j0 + cols_per);
   unsigned long long mx[4] = {0, 0, 0, 0};
   const bool vec = i0 + 4 <= m && (ldw & 3) == 0 && (reinterpret_cast<uintptr_t>(W + b * w_stride) & 15) == 0;
   if (vec) {
@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(256) k_stc_rowmax(const TW *W, int64_t ldw, in
 // every CTA of the column from L2), then the 7 balanced digits of its 256 entries into the
 // canonical B tiles [nt][ks][slice][t, k] (zero beyond n and lbar).
 template <int NP>
-__global__ void __launch_bounds__(256) k_stc_omega(const double *omega, int64_t ldo, int64_t n, int64_t lbar,
-                                                   int64_t KS, signed char *od, int *fexp) {
-  const int nt = blockIdx.x / NP, t = blockIdx.x % NP;
+__device__ __forceinline__ void stc_omega(const double *omega, int64_t ldo, int64_t n, int64_t lbar, int64_t KS,
+                                          signed char *od, int *fexp, int64_t bx, int64_t by) {
+  const int nt = (int)(bx / NP), t = (int)(bx % NP);
   const int64_t c = (int64_t)nt * NP + t;                    // column of Omega (padding beyond lbar)
   const bool live = c < lbar;
   const double *col = omega + c * ldo;
@@ -262,15 +262,32 @@ __global__ void __launch_bounds__(256) k_stc_omega(const double *omega, int64_t 
     f = ilogb(mx) + 1;
     if (mx >= ldexp(127.0 / 128.0, f)) ++f;
   }
-  if (threadIdx.x == 0 && blockIdx.y == 0) fexp[c] = f;
+  if (threadIdx.x == 0 && by == 0) fexp[c] = f;
   const double sc = ldexp(1.0, 55 - f);
-  const int64_t j = (int64_t)blockIdx.y * 8 * BK + threadIdx.x;
+  const int64_t j = by * 8 * BK + threadIdx.x;
   if (j >= KS * BK) return;
   const double v = (live && j < n) ? __ldg(col + j) : 0.0;
   const unsigned long long B = (unsigned long long)__double2ll_rn(v * sc) + 0x0080808080808080ull;
   signed char *tile = od + ((size_t)nt * KS + j / BK) * S * (NP * BK) + tc::canon_off(t, (int)(j % BK));
 #pragma unroll
   for (int s = 0; s < S; ++s) tile[(size_t)s * (NP * BK)] = (signed char)((int)((B >> (8 * (6 - s))) & 0xffu) - 128);
+}
+
+// ---------------------------------------------------------------- the prologue in one launch
+// blocks [0, R): row maxima (R = RB x CS x nb), blocks [R, R + O): Omega digits (O = NTN NP x KSB)
+template <typename TW, int NP>
+__global__ void __launch_bounds__(256) k_stc_prep(const TW *W, int64_t ldw, int64_t w_stride, int64_t m, int64_t n,
+                                                  int64_t cols_per, int64_t RB, int64_t CS, int64_t nbr,
+                                                  unsigned long long *rowmax, const double *omega, int64_t ldo,
+                                                  int64_t lbar, int64_t KS, int64_t KSB, signed char *od, int *fexp) {
+  const int64_t blk = blockIdx.x;
+  if (blk < nbr) {
+    const int64_t bx = blk % RB, by = (blk / RB) % CS, b = blk / (RB * CS);
+    stc_rowmax<TW>(W, ldw, w_stride, m, n, cols_per, rowmax, bx, by, b);
+  } else {
+    const int64_t o = blk - nbr;
+    stc_omega<NP>(omega, ldo, n, lbar, KS, od, fexp, o / KSB, o % KSB);
+  }
 }
 
 // ---------------------------------------------------------------- main kernel
@@ -668,7 +685,7 @@ size_t sketch_tc_zero_bytes() { return stc::plan(1, 1, 1, 1).off_rowmax; }
 
 // Y = W * Omega (m x lbar, fp64) on the tensor cores for nb problems sharing Omega (dense fp32 /
 // fp64 W, column-major, ldw, w_stride; Omega n x lbar column-major fp64, ldo).  scratch: at least
-// sketch_tc_scratch_bytes(m, n, lbar, nb), 256-byte aligned.  Three launches plus one memset.
+// sketch_tc_scratch_bytes(m, n, lbar, nb), 256-byte aligned.  Two launches plus one memset.
 cudaError_t launch_sketch_tc(const SketchArgs &sa, int64_t nb, const double *omega, int64_t ldo, void *scratch,
                              size_t scratch_bytes, cudaStream_t st, Prof *pf) {
   using namespace stc;
@@ -724,22 +741,25 @@ cudaError_t launch_sketch_tc(const SketchArgs &sa, int64_t nb, const double *ome
     int64_t CS = (2 * sm_count() + RB * nb - 1) / (RB * nb);  // ~two CTAs per SM, 128 KB in flight
     CS = std::max<int64_t>(1, std::min<int64_t>(CS, (sa.n + 15) / 16));
     const int64_t cols_per = (sa.n + CS - 1) / CS;
-    const dim3 g((unsigned)RB, (unsigned)((sa.n + cols_per - 1) / cols_per), (unsigned)nb);
+    const int64_t CSr = (sa.n + cols_per - 1) / cols_per;
+    const int64_t nbr = RB * CSr * nb, KSB = (p.KS + 7) / 8, nbo = p.NTN * p.NP * KSB;
     unsigned long long *rm = const_cast<unsigned long long *>(a.rowmax);
-    if (sa.dtype == LRA_F32)
-      k_stc_rowmax<float><<<g, 256, 0, st>>>(reinterpret_cast<const float *>(sa.w), sa.ldw, sa.w_stride, sa.m, sa.n,
-                                             cols_per, rm);
-    else
-      k_stc_rowmax<double><<<g, 256, 0, st>>>(reinterpret_cast<const double *>(sa.w), sa.ldw, sa.w_stride, sa.m, sa.n,
-                                              cols_per, rm);
     signed char *od = const_cast<signed char *>(a.od);
     int *fx = const_cast<int *>(a.fexp);
-    const dim3 nbk((unsigned)(p.NTN * p.NP), (unsigned)((p.KS + 7) / 8));
-    switch (p.NP) {
-      case 16: k_stc_omega<16><<<nbk, 256, 0, st>>>(omega, ldo, sa.n, sa.lbar, p.KS, od, fx); break;
-      case 32: k_stc_omega<32><<<nbk, 256, 0, st>>>(omega, ldo, sa.n, sa.lbar, p.KS, od, fx); break;
-      default: k_stc_omega<48><<<nbk, 256, 0, st>>>(omega, ldo, sa.n, sa.lbar, p.KS, od, fx); break;
+    const unsigned grid = (unsigned)(nbr + nbo);
+#define STC_PREP(TW, NPV)                                                                                       \
+  k_stc_prep<TW, NPV><<<grid, 256, 0, st>>>(reinterpret_cast<const TW *>(sa.w), sa.ldw, sa.w_stride, sa.m, sa.n, \
+                                            cols_per, RB, CSr, nbr, rm, omega, ldo, sa.lbar, p.KS, KSB, od, fx)
+    if (sa.dtype == LRA_F32) {
+      if (p.NP == 16) STC_PREP(float, 16);
+      else if (p.NP == 32) STC_PREP(float, 32);
+      else STC_PREP(float, 48);
+    } else {
+      if (p.NP == 16) STC_PREP(double, 16);
+      else if (p.NP == 32) STC_PREP(double, 32);
+      else STC_PREP(double, 48);
     }
+#undef STC_PREP
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   pf->end(st);
