@@ -28,8 +28,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     from concurrent.futures import ThreadPoolExecutor
 
+    # LRA_KEEP_OBJ=1 (development): objects are kept under build/ and a translation unit is
+    # recompiled only when it, or any header, is newer than its object
+    keep = os.environ.get("LRA_KEEP_OBJ") == "1"
+    odir = os.path.join(HERE, "..", "build", "obj" + os.environ.get("LRA_OBJ_TAG", "")) if keep else CSRC
+    os.makedirs(odir, exist_ok=True)
+    hdr = max([os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] +
+              [os.path.getmtime(os.path.join(HERE, "..", "include", "lra.h"))])
+
     def compile_one(src):
-        obj = os.path.join(CSRC, src.replace(".cu", (os.environ.get("LRA_OBJ_TAG", "") + ".o")))
+        obj = os.path.join(odir, src.replace(".cu", (os.environ.get("LRA_OBJ_TAG", "") + ".o")))
+        if keep and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr, os.path.getmtime(os.path.join(CSRC, src))):
+            return src, obj, subprocess.CompletedProcess([], 0, "", "")
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
@@ -54,8 +64,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    for o in objs:
-        os.remove(o)
+    if not keep:
+        for o in objs:
+            os.remove(o)
     return SO
 
 

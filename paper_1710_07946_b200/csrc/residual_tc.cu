@@ -69,6 +69,9 @@ template <int S> struct Tr;
 // issuers reach the M=128 N=32 math floor of 16), so the S(S+1)/2 products of a tile are spread
 // over several warps by level: PRECISE levels {0,1,2,3} {4,5} = 10, 11 products (20 warps in
 // all, a multiple of 4, keep 96 registers per thread for the epilogue).
+#ifndef RTC_PREC_NMW
+#define RTC_PREC_NMW 3    // MMA-issuing warps, PRECISE (3: 345 vs 355 us on 16384^2)
+#endif
 #ifndef RTC_PREC_G
 #define RTC_PREC_G 2      // epilogue groups, PRECISE (diagnostic builds may override)
 #endif
@@ -76,11 +79,23 @@ template <int S> struct Tr;
 #define RTC_FAST_G 2      // epilogue groups, FAST
 #endif
 template <> struct Tr<6> {
-  static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 2, G = RTC_PREC_G;
+#if RTC_PREC_NMW == 3
+  // three issuers: levels {5} {4, 0} {3, 2, 1} = 6, 6, 9 products
+  static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 3, G = RTC_PREC_G, XW = 4;
+  static constexpr int warp_of(int l) { return l == 5 ? 0 : (l == 4 || l == 0) ? 1 : 2; }
+#else
+  static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 2, G = RTC_PREC_G, XW = 8;
   static constexpr int warp_of(int l) { return l <= 3 ? 0 : 1; }
+#endif
 };
+#ifndef RTC_FAST_BN
+#define RTC_FAST_BN 64    // FAST tile width (diagnostic builds: 32 with 4 accumulator buffers)
+#endif
+#ifndef RTC_FAST_NBUF
+#define RTC_FAST_NBUF 2
+#endif
 template <> struct Tr<3> {
-  static constexpr int BN = 64, TPI = 8, NBUF = 2, NMW = 2, G = RTC_FAST_G;
+  static constexpr int BN = RTC_FAST_BN, TPI = 512 / RTC_FAST_BN, NBUF = RTC_FAST_NBUF, NMW = 2, G = RTC_FAST_G, XW = 8;
   static constexpr int warp_of(int l) { return l <= 1 ? 0 : 1; }
 };
 template <int S> constexpr int nthreads() { return 32 * (NE + 2 + Tr<S>::NMW); }
@@ -295,8 +310,10 @@ struct TcArgs {
   int KB;
   int64_t RB, CB;                 // row blocks, BN-column tiles per problem
   int64_t nchunk;                 // column chunks (items) per row block
+  int tpi;                        // tiles per item (a multiple of Tr<S>::TPI, see launch_residual_tc)
   int64_t items;                  // nb * RB * nchunk
   int nabuf;                      // TMEM A regions (2: double-buffered across items, 1: single)
+  int nas;                        // shared-memory A buffers (TS mode: 1 — A leaves for TMEM at once; SS: 2)
   int nws;                        // W stages (<= NWS)
   int nbs;                        // B-slice stages (<= NBS)
   double2 *partial;               // per problem: RB * nchunk partials (one per work item)
@@ -308,14 +325,29 @@ struct Bars {
       aempty[2], astaged[2], aread[2];
 };
 
-template <int S, int BN>
-__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&P)[S][8]) {
+// levels 0 .. S-1 of XW (4 or 8) consecutive accumulator columns, 32 lanes (32x32b shape)
+template <int S, int BN, int XW>
+__device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&P)[S][XW]) {
+#pragma unroll
+  for (int l = 0; l < S; ++l) {
+    if constexpr (XW == 8)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(P[l][0]), "=r"(P[l][1]), "=r"(P[l][2]), "=r"(P[l][3]), "=r"(P[l][4]), "=r"(P[l][5]),
+                     "=r"(P[l][6]), "=r"(P[l][7])
+                   : "r"(addr + (uint32_t)(l * BN)));
+    else
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(P[l][0]), "=r"(P[l][1]), "=r"(P[l][2]), "=r"(P[l][3])
+                   : "r"(addr + (uint32_t)(l * BN)));
+  }
+}
+// register dependence on a tcgen05.wait::ld: no use of P is scheduled before the wait
+template <int S, int XW>
+__device__ __forceinline__ void reg_dep(uint32_t (&P)[S][XW]) {
 #pragma unroll
   for (int l = 0; l < S; ++l)
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(P[l][0]), "=r"(P[l][1]), "=r"(P[l][2]), "=r"(P[l][3]), "=r"(P[l][4]), "=r"(P[l][5]),
-                   "=r"(P[l][6]), "=r"(P[l][7])
-                 : "r"(addr + (uint32_t)(l * BN)));
+#pragma unroll
+    for (int x = 0; x < XW; ++x) asm volatile("" : "+r"(P[l][x]));
 }
 
 // The MMAs of MMA warp MW for one tile: round j issues product j of every level l >= j that the
@@ -343,7 +375,8 @@ __device__ __forceinline__ void issue_tile(uint32_t dbase, uint32_t at, uint64_t
 template <int S, bool TS, int KB>
 __device__ __forceinline__ void issue_tile_mw(int mw, uint32_t dbase, uint32_t at, uint64_t adesc, uint64_t bdesc) {
   if (mw == 0) issue_tile<S, 0, TS, KB>(dbase, at, adesc, bdesc);
-  else issue_tile<S, 1, TS, KB>(dbase, at, adesc, bdesc);
+  else if (Tr<S>::NMW < 3 || mw == 1) issue_tile<S, 1, TS, KB>(dbase, at, adesc, bdesc);
+  else issue_tile<S, 2, TS, KB>(dbase, at, adesc, bdesc);
 }
 
 // Persistent, warp-specialized.  Work item = (problem, row block, chunk of TPI tiles).
@@ -352,7 +385,7 @@ __device__ __forceinline__ void issue_tile_mw(int mw, uint32_t dbase, uint32_t a
 template <typename TW, int S, bool TS>
 __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constant__ TcArgs a,
                                                            const __grid_constant__ CUtensorMap tmW) {
-  constexpr int BN = Tr<S>::BN, TPI = Tr<S>::TPI, NBUF = Tr<S>::NBUF, NMW = Tr<S>::NMW, GG = Tr<S>::G;
+  constexpr int BN = Tr<S>::BN, NBUF = Tr<S>::NBUF, NMW = Tr<S>::NMW, GG = Tr<S>::G;
   constexpr int B_TILE = BN * BK;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) Bars bar;
@@ -363,7 +396,7 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int aBytes = S * KB * A_TILE, bBytes = S * KB * B_TILE;
   unsigned char *As = smem;                              // 2 item buffers
-  unsigned char *Bst = As + 2 * aBytes;                  // NBS stages
+  unsigned char *Bst = As + a.nas * aBytes;              // NBS stages
   TW *Wst = reinterpret_cast<TW *>(Bst + a.nbs * bBytes);  // nws stages of BN columns x 128 rows
   const uint32_t bb = smem_u32(&bar);
   const uint32_t B_WFULL = bb + offsetof(Bars, wfull), B_WEMPTY = bb + offsetof(Bars, wempty);
@@ -405,13 +438,22 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
   const uint32_t abase_t = tmem + (uint32_t)(NBUF * S * BN);   // A regions: 8 columns per (kb, slice)
   const uint32_t aregion = (uint32_t)(S * KB * 8);
 
+  const bool small_items = a.items < (1ll << 31);   // 32-bit index arithmetic (64-bit division is ~70 instructions)
   auto item_of = [&](int64_t it, int64_t &b, int64_t &rb, int64_t &c0, int64_t &c1) {
-    b = it / (a.RB * a.nchunk);
-    const int64_t rem = it % (a.RB * a.nchunk);
-    const int64_t ch = rem / a.RB;
-    rb = rem % a.RB;
-    c0 = ch * TPI;
-    c1 = min(c0 + (int64_t)TPI, a.CB);
+    int64_t ch;
+    if (small_items) {
+      const uint32_t per = (uint32_t)(a.RB * a.nchunk), i32 = (uint32_t)it, rem = i32 % per;
+      b = i32 / per;
+      ch = rem / (uint32_t)a.RB;
+      rb = rem % (uint32_t)a.RB;
+    } else {
+      b = it / (a.RB * a.nchunk);
+      const int64_t rem = it % (a.RB * a.nchunk);
+      ch = rem / a.RB;
+      rb = rem % a.RB;
+    }
+    c0 = ch * a.tpi;
+    c1 = min(c0 + (int64_t)a.tpi, a.CB);
   };
 
   if (warp == NE) {
@@ -422,9 +464,9 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
       int64_t b, rb, c0, c1;
       item_of(it, b, rb, c0, c1);
       if (a.status && a.status[b] != LRA_OK) continue;
-      const int ab = (int)(ni & 1);
+      const int ab = a.nas == 2 ? (int)(ni & 1) : 0;
       long long t0 = RTC_CLK();
-      if (ni >= 2) mbar_wait(B_AEMPTY + 8 * ab, (uint32_t)(((ni >> 1) - 1) & 1));
+      if (ni >= a.nas) mbar_wait(B_AEMPTY + 8 * ab, (uint32_t)(((ni / a.nas) - 1) & 1));
       pw_a += RTC_CLK() - t0;
       ++ni;
       if (elect_one()) {
@@ -483,14 +525,15 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
       int64_t b, rb, c0, c1;
       item_of(it, b, rb, c0, c1);
       if (a.status && a.status[b] != LRA_OK) continue;
-      const int ab = (int)(ni & 1);
-      const int ar = a.nabuf == 2 ? ab : 0;                      // TMEM A region of this item
+      const int ab = a.nas == 2 ? (int)(ni & 1) : 0;            // shared-memory A buffer
+      const uint32_t aph = (uint32_t)((ni / a.nas) & 1);
+      const int ar = a.nabuf == 2 ? (int)(ni & 1) : 0;          // TMEM A region of this item
       const int64_t use = a.nabuf == 2 ? (ni >> 1) : ni;        // use count of that region
       long long t0 = RTC_CLK();
       if (TS) {
         if (mw == 0) {
           if (use >= 1) mbar_wait(B_AREAD + 8 * ar, (uint32_t)((use - 1) & 1));
-          mbar_wait(B_AFULL + 8 * ab, (uint32_t)((ni >> 1) & 1));
+          mbar_wait(B_AFULL + 8 * ab, aph);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           if (elect_one()) {
             const uint64_t adesc = smem_desc(smem_u32(As + ab * aBytes));
@@ -504,7 +547,7 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
           mbar_wait(B_ASTG + 8 * ar, (uint32_t)(use & 1));
         }
       } else {
-        mbar_wait(B_AFULL + 8 * ab, (uint32_t)((ni >> 1) & 1));
+        mbar_wait(B_AFULL + 8 * ab, aph);
       }
       mw_a += RTC_CLK() - t0;
       ++ni;
@@ -553,7 +596,7 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
     // group, warp q4 = warp % 4 reads TMEM lanes 32 q4 .. (its 32 rows) and the column slice cs
     // (BN / NCS columns, chunks of 8) for all S levels.  Branch-free: rows and columns beyond the
     // problem hold zero W (TMA fill), zero digits (split) and a zero scale, so they add nothing.
-    constexpr int WPG = NE / GG, NCS = WPG / 4, CW = BN / NCS, NCH = CW / 8;
+    constexpr int WPG = NE / GG, NCS = WPG / 4, CW = BN / NCS, XW = Tr<S>::XW, NCH = CW / XW;
     const int grp = warp / WPG, q4 = warp & 3, cs = (warp % WPG) >> 2;
     const int rl = 32 * q4 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(CW * cs);
@@ -582,15 +625,15 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
         long long te1 = RTC_CLK();
         ew_t += te1 - te0;
         const TW *wt = Wst + (size_t)wsg * BM * BN + (size_t)(CW * cs) * BM + rl;
+        const uint32_t tbase = lane_addr + (uint32_t)(tb * S * BN);
+        // (measured: loading chunk c + 1 ahead of chunk c's arithmetic does not help — the drain
+        // is not TMEM-latency bound — and costs the registers of a second chunk)
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          uint32_t P[S][8];
-          tmem_ld8<S, BN>(lane_addr + (uint32_t)(tb * S * BN + 8 * c), P);
+          uint32_t Q[S][XW];
+          tmem_ld<S, BN, XW>(tbase + (uint32_t)(XW * c), Q);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-          for (int l = 0; l < S; ++l)   // register dependence on the wait: no use before it
-            asm volatile("" : "+r"(P[l][0]), "+r"(P[l][1]), "+r"(P[l][2]), "+r"(P[l][3]), "+r"(P[l][4]),
-                         "+r"(P[l][5]), "+r"(P[l][6]), "+r"(P[l][7]));
+          reg_dep<S, XW>(Q);
           if (c == NCH - 1) {           // every chunk read: release the TMEM buffer to the MMA warps
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
@@ -602,20 +645,28 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
             ew_w += RTC_CLK() - tw0;
           }
 #pragma unroll
-          for (int x = 0; x < 8; ++x) {
+          for (int x = 0; x < XW; ++x) {
             // R: the recombined levels as an exact int64 (|R| < 2^51), converted to fp64 by the
             // 1.5 2^52 magic add (integer + fp64 pipes: no XU conversion; profiling showed the XU
             // pipe, 16 ops/clk/SM, bounding the I2F-based version)
-            long long R;
-            if (S == 6) {   // R = 2^16 (256 P0 + P1) + (256 P2 + P3) + floor(P4 / 2^8) + floor(P5 / 2^16)
-              const int b1 = (int)P[0][x] * 256 + (int)P[1][x];
-              const int c = (int)P[2][x] * 256 + (int)P[3][x] + ((int)P[4][x] >> 8) + ((int)P[5][x] >> 16);
-              R = (long long)b1 * 65536ll + (long long)c;     // the floors: < 2 units = 2^-43 of |R|max
-            } else {        // R = 2^16 P0 + 256 P1 + P2
-              R = (long long)(int)P[0][x] * 65536ll + (long long)((int)P[1][x] * 256 + (int)P[2][x]);
+            // R = 2^16 b1 + lo with
+            //   PRECISE b1 = 256 P0 + P1, lo = (256 P2 + P3) + floor(P4 / 2^8) + floor(P5 / 2^16)
+            //           (the floors: < 2 units = 2^-43 of |R|max)
+            //   FAST    b1 = P0,          lo = 256 P1 + P2.
+            // R + 0x4338000000000000 is one wide multiply-add: the magic only touches the high
+            // word, so the addend is the pair (lo, sign(lo) + 0x43380000) — no 64-bit adds.
+            int b1, lo;
+            if (S == 6) {
+              b1 = (int)Q[0][x] * 256 + (int)Q[1][x];
+              lo = (int)Q[2][x] * 256 + (int)Q[3][x] + ((int)Q[4][x] >> 8) + ((int)Q[5][x] >> 16);
+            } else {
+              b1 = (int)Q[0][x];
+              lo = (int)Q[1][x] * 256 + (int)Q[2][x];
             }
-            const double u = __longlong_as_double(R + 0x4338000000000000LL) - 6755399441055744.0;
-            const double wd = (double)wt[(8 * c + x) * BM];
+            const long long cm = (long long)(((unsigned long long)(unsigned)((lo >> 31) + 0x43380000) << 32) |
+                                             (unsigned long long)(unsigned)lo);
+            const double u = __longlong_as_double((long long)b1 * 65536ll + cm) - 6755399441055744.0;
+            const double wd = (double)wt[(XW * c + x) * BM];
             const double d = fma(-u, sc, wd);
             nu[x & 3] = fma(d, d, nu[x & 3]);
             de[x & 3] = fma(wd, wd, de[x & 3]);
@@ -765,7 +816,14 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
   t.KB = KB;
   t.RB = RB;
   t.CB = CB;
-  t.nchunk = (CB + TPI - 1) / TPI;
+  // Tiles per item: the base TPI, doubled (up to 8x) while every SM still gets >= 8 items.
+  // Longer items amortise the per-item work (the A slices' load and TMEM copy, the exponent
+  // loads, the 16 warps' partial sums): 32768^2 r = 64 FAST 949 -> see DESIGN.md §6.2.
+  static const int tpi_max = getenv("LRA_RTC_TPIX") ? atoi(getenv("LRA_RTC_TPIX")) : 8;   // diagnostics
+  int tpi = TPI;
+  while (tpi < tpi_max * TPI && nb * RB * ((CB + 2 * tpi - 1) / (2 * tpi)) >= 8 * (int64_t)num_sms_rtc()) tpi *= 2;
+  t.tpi = tpi;
+  t.nchunk = (CB + tpi - 1) / tpi;
   t.items = nb * RB * t.nchunk;
   const size_t elt = a.dtype == LRA_F32 ? 4 : 8;
   // W through a TMA tensor map over (m, n, nb) when the strides allow it (16-byte multiples)
@@ -795,16 +853,29 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
   }
   t.partial = a.partial;
   t.status = a.status;
+  t.nas = ts_mode ? 1 : 2;
   auto smem_of = [&](int nws, int nbs) {
-    return 2 * (size_t)S * KB * A_TILE + (size_t)nbs * S * KB * BN * BK + (size_t)nws * BM * BN * elt;
+    return (size_t)t.nas * S * KB * A_TILE + (size_t)nbs * S * KB * BN * BK + (size_t)nws * BM * BN * elt;
   };
+  // W stages first (the HBM stream the kernel is bound by), then B stages (L2-resident slices):
+  // the first (nws, nbs) in (4, 2) x (8, 4, 2) that fits.  r = 64 FAST gets 4 W stages instead
+  // of 2.  More than 4 W stages does not pay: PRECISE r = 32 at 8 W stages (200 KB of shared
+  // memory) is no faster alone and, in lra_batch, keeps the next group's nucleus and factor CTAs
+  // off the SMs (config-2 bench 9395 -> 8393 matrices/s).
   const size_t lim = 227 * 1024 - 4096;
-  t.nws = NWS;
-  t.nbs = NBS;
-  if (smem_of(t.nws, t.nbs) > lim) t.nws = 4;
-  if (smem_of(t.nws, t.nbs) > lim) t.nbs = 4;
-  if (smem_of(t.nws, t.nbs) > lim) t.nws = 2;
-  if (smem_of(t.nws, t.nbs) > lim) t.nbs = 2;
+  t.nws = 2;
+  t.nbs = 2;
+  {
+    bool found = false;
+    static const int nws_max = getenv("LRA_RTC_NWS") ? atoi(getenv("LRA_RTC_NWS")) : 4;   // diagnostics
+    for (int w = nws_max; w >= 2 && !found; w >>= 1)
+      for (int b = NBS; b >= 2 && !found; b >>= 1)
+        if (smem_of(w, b) <= lim) {
+          t.nws = w;
+          t.nbs = b;
+          found = true;
+        }
+  }
   const size_t smem = smem_of(t.nws, t.nbs);
   if (smem > lim) return cudaErrorInvalidConfiguration;   // caller falls back to the fp64 SIMT pass
   const int64_t grid = t.items < num_sms_rtc() ? t.items : num_sms_rtc();
