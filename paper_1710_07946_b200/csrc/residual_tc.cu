@@ -69,8 +69,11 @@ template <int S> struct Tr;
 // issuers reach the M=128 N=32 math floor of 16), so the S(S+1)/2 products of a tile are spread
 // over several warps by level: PRECISE levels {0,1,2,3} {4,5} = 10, 11 products (20 warps in
 // all, a multiple of 4, keep 96 registers per thread for the epilogue).
+#ifndef RTC_PREC_EARLY
+#define RTC_PREC_EARLY 1  // PRECISE: drain TMEM, release, then the fp64 work
+#endif
 #ifndef RTC_PREC_NMW
-#define RTC_PREC_NMW 3    // MMA-issuing warps, PRECISE (3: 345 vs 355 us on 16384^2)
+#define RTC_PREC_NMW 2    // MMA-issuing warps, PRECISE (3 issuers: 80 registers, the early drain spills)
 #endif
 #ifndef RTC_PREC_G
 #define RTC_PREC_G 2      // epilogue groups, PRECISE (diagnostic builds may override)
@@ -82,9 +85,11 @@ template <> struct Tr<6> {
 #if RTC_PREC_NMW == 3
   // three issuers: levels {5} {4, 0} {3, 2, 1} = 6, 6, 9 products
   static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 3, G = RTC_PREC_G, XW = 4;
+  static constexpr bool EARLY = RTC_PREC_EARLY;
   static constexpr int warp_of(int l) { return l == 5 ? 0 : (l == 4 || l == 0) ? 1 : 2; }
 #else
   static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 2, G = RTC_PREC_G, XW = 8;
+  static constexpr bool EARLY = RTC_PREC_EARLY;
   static constexpr int warp_of(int l) { return l <= 3 ? 0 : 1; }
 #endif
 };
@@ -96,6 +101,7 @@ template <> struct Tr<6> {
 #endif
 template <> struct Tr<3> {
   static constexpr int BN = RTC_FAST_BN, TPI = 512 / RTC_FAST_BN, NBUF = RTC_FAST_NBUF, NMW = 2, G = RTC_FAST_G, XW = 8;
+  static constexpr bool EARLY = false;
   static constexpr int warp_of(int l) { return l <= 1 ? 0 : 1; }
 };
 template <int S> constexpr int nthreads() { return 32 * (NE + 2 + Tr<S>::NMW); }
@@ -626,50 +632,80 @@ __global__ void __launch_bounds__(nthreads<S>(), 1) k_resid(const __grid_constan
         ew_t += te1 - te0;
         const TW *wt = Wst + (size_t)wsg * BM * BN + (size_t)(CW * cs) * BM + rl;
         const uint32_t tbase = lane_addr + (uint32_t)(tb * S * BN);
-        // (measured: loading chunk c + 1 ahead of chunk c's arithmetic does not help — the drain
-        // is not TMEM-latency bound — and costs the registers of a second chunk)
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          uint32_t Q[S][XW];
-          tmem_ld<S, BN, XW>(tbase + (uint32_t)(XW * c), Q);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          reg_dep<S, XW>(Q);
-          if (c == NCH - 1) {           // every chunk read: release the TMEM buffer to the MMA warps
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(B_TEMPTY + 8 * tb);
+        // R: the recombined levels as an exact int64 (|R| < 2^51), converted to fp64 by the
+        // 1.5 2^52 magic add (integer + fp64 pipes: no XU conversion; profiling showed the XU
+        // pipe, 16 ops/clk/SM, bounding the I2F-based version).  R = 2^16 b1 + lo with
+        //   PRECISE b1 = 256 P0 + P1, lo = (256 P2 + P3) + floor(P4 / 2^8) + floor(P5 / 2^16)
+        //           (the floors: < 2 units = 2^-43 of |R|max)
+        //   FAST    b1 = P0,          lo = 256 P1 + P2.
+        // R + 0x4338000000000000 is one wide multiply-add: the magic only touches the high word,
+        // so the addend is the pair (lo, sign(lo) + 0x43380000) — no 64-bit adds.
+        auto combine = [&](const uint32_t (&Q)[S][XW], int x, int &b1, int &lo) {
+          if (S == 6) {
+            b1 = (int)Q[0][x] * 256 + (int)Q[1][x];
+            lo = (int)Q[2][x] * 256 + (int)Q[3][x] + ((int)Q[4][x] >> 8) + ((int)Q[5][x] >> 16);
+          } else {
+            b1 = (int)Q[0][x];
+            lo = (int)Q[1][x] * 256 + (int)Q[2][x];
           }
-          if (c == 0) {
-            long long tw0 = RTC_CLK();
-            mbar_wait(B_WFULL + 8 * wsg, (uint32_t)((k >> wsh) & 1));
-            ew_w += RTC_CLK() - tw0;
-          }
+        };
+        auto accumulate = [&](int b1, int lo, int col, int x) {
+          const long long cm = (long long)(((unsigned long long)(unsigned)((lo >> 31) + 0x43380000) << 32) |
+                                           (unsigned long long)(unsigned)lo);
+          const double u = __longlong_as_double((long long)b1 * 65536ll + cm) - 6755399441055744.0;
+          const double wd = (double)wt[col * BM];
+          const double d = fma(-u, sc, wd);
+          nu[x & 3] = fma(d, d, nu[x & 3]);
+          de[x & 3] = fma(wd, wd, de[x & 3]);
+        };
+        if constexpr (Tr<S>::EARLY) {
+          // PRECISE: drain the whole TMEM slice first (levels combined into (b1, lo) pairs as
+          // they arrive), release the buffer, then the fp64 work — the MMAs of the next tile
+          // into this buffer overlap the arithmetic instead of waiting for it (the MMA side,
+          // 21 products per tile, is what the epilogue waited on: TFULL stalls)
+          int B1[CW], LO[CW];
 #pragma unroll
-          for (int x = 0; x < XW; ++x) {
-            // R: the recombined levels as an exact int64 (|R| < 2^51), converted to fp64 by the
-            // 1.5 2^52 magic add (integer + fp64 pipes: no XU conversion; profiling showed the XU
-            // pipe, 16 ops/clk/SM, bounding the I2F-based version)
-            // R = 2^16 b1 + lo with
-            //   PRECISE b1 = 256 P0 + P1, lo = (256 P2 + P3) + floor(P4 / 2^8) + floor(P5 / 2^16)
-            //           (the floors: < 2 units = 2^-43 of |R|max)
-            //   FAST    b1 = P0,          lo = 256 P1 + P2.
-            // R + 0x4338000000000000 is one wide multiply-add: the magic only touches the high
-            // word, so the addend is the pair (lo, sign(lo) + 0x43380000) — no 64-bit adds.
-            int b1, lo;
-            if (S == 6) {
-              b1 = (int)Q[0][x] * 256 + (int)Q[1][x];
-              lo = (int)Q[2][x] * 256 + (int)Q[3][x] + ((int)Q[4][x] >> 8) + ((int)Q[5][x] >> 16);
-            } else {
-              b1 = (int)Q[0][x];
-              lo = (int)Q[1][x] * 256 + (int)Q[2][x];
+          for (int c = 0; c < NCH; ++c) {
+            uint32_t Q[S][XW];
+            tmem_ld<S, BN, XW>(tbase + (uint32_t)(XW * c), Q);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            reg_dep<S, XW>(Q);
+#pragma unroll
+            for (int x = 0; x < XW; ++x) combine(Q, x, B1[XW * c + x], LO[XW * c + x]);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(B_TEMPTY + 8 * tb);
+          long long tw0 = RTC_CLK();
+          mbar_wait(B_WFULL + 8 * wsg, (uint32_t)((k >> wsh) & 1));
+          ew_w += RTC_CLK() - tw0;
+#pragma unroll
+          for (int x = 0; x < CW; ++x) accumulate(B1[x], LO[x], x, x);
+        } else {
+          // FAST: chunk by chunk (loading chunk c + 1 ahead of chunk c's arithmetic was measured:
+          // no gain — the drain is not TMEM-latency bound — for the registers of a second chunk)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            uint32_t Q[S][XW];
+            tmem_ld<S, BN, XW>(tbase + (uint32_t)(XW * c), Q);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            reg_dep<S, XW>(Q);
+            if (c == NCH - 1) {           // every chunk read: release the TMEM buffer to the MMA warps
+              asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+              __syncwarp();
+              if (lane == 0) mbar_arrive(B_TEMPTY + 8 * tb);
             }
-            const long long cm = (long long)(((unsigned long long)(unsigned)((lo >> 31) + 0x43380000) << 32) |
-                                             (unsigned long long)(unsigned)lo);
-            const double u = __longlong_as_double((long long)b1 * 65536ll + cm) - 6755399441055744.0;
-            const double wd = (double)wt[(XW * c + x) * BM];
-            const double d = fma(-u, sc, wd);
-            nu[x & 3] = fma(d, d, nu[x & 3]);
-            de[x & 3] = fma(wd, wd, de[x & 3]);
+            if (c == 0) {
+              long long tw0 = RTC_CLK();
+              mbar_wait(B_WFULL + 8 * wsg, (uint32_t)((k >> wsh) & 1));
+              ew_w += RTC_CLK() - tw0;
+            }
+#pragma unroll
+            for (int x = 0; x < XW; ++x) {
+              int b1, lo;
+              combine(Q, x, b1, lo);
+              accumulate(b1, lo, XW * c + x, x);
+            }
           }
         }
         __syncwarp();
