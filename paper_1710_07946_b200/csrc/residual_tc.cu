@@ -72,26 +72,31 @@ template <int S> struct Tr;
 #ifndef RTC_PREC_EARLY
 #define RTC_PREC_EARLY 1  // PRECISE: drain TMEM, release, then the fp64 work
 #endif
-#ifndef RTC_PREC_NMW
-#define RTC_PREC_NMW 2    // MMA-issuing warps, PRECISE (3 issuers: 80 registers, the early drain spills)
-#endif
 #ifndef RTC_PREC_G
-#define RTC_PREC_G 2      // epilogue groups, PRECISE (diagnostic builds may override)
+#define RTC_PREC_G 1      // epilogue groups, PRECISE (one buffer: all 16 warps drain each tile)
+#endif
+#ifndef RTC_PREC_BN
+#define RTC_PREC_BN 64    // PRECISE tile width and accumulator buffers (6 levels x BN columns each):
+                          // 64 columns with ONE buffer (384 TMEM columns) halves the MMAs per byte
+                          // of W against 32 x 2 buffers; the early drain releases the buffer before
+                          // the fp64 work (16384^2 334 -> 320 us, config-2 bench +1.4 %)
+#endif
+#ifndef RTC_PREC_SMEM_KB
+#define RTC_PREC_SMEM_KB 140
+#endif
+#ifndef RTC_PREC_NBUF
+#define RTC_PREC_NBUF 1
 #endif
 #ifndef RTC_FAST_G
 #define RTC_FAST_G 2      // epilogue groups, FAST
 #endif
 template <> struct Tr<6> {
-#if RTC_PREC_NMW == 3
-  // three issuers: levels {5} {4, 0} {3, 2, 1} = 6, 6, 9 products
-  static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 3, G = RTC_PREC_G, XW = 4;
-  static constexpr bool EARLY = RTC_PREC_EARLY;
-  static constexpr int warp_of(int l) { return l == 5 ? 0 : (l == 4 || l == 0) ? 1 : 2; }
-#else
-  static constexpr int BN = 32, TPI = 16, NBUF = 2, NMW = 2, G = RTC_PREC_G, XW = 8;
+  static constexpr int BN = RTC_PREC_BN, TPI = 512 / RTC_PREC_BN, NBUF = RTC_PREC_NBUF, NMW = 2, G = RTC_PREC_G, XW = 8;
   static constexpr bool EARLY = RTC_PREC_EARLY;
   static constexpr int warp_of(int l) { return l <= 3 ? 0 : 1; }
-#endif
+  // shared-memory budget: PRECISE runs inside lra_batch next to the nucleus / factor CTAs of
+  // other groups, and a 200 KB CTA keeps them off its SM (config-2 bench 9395 -> 8393)
+  static constexpr size_t SMEM_CAP = (size_t)RTC_PREC_SMEM_KB * 1024;
 };
 #ifndef RTC_FAST_BN
 #define RTC_FAST_BN 64    // FAST tile width (diagnostic builds: 32 with 4 accumulator buffers)
@@ -103,6 +108,7 @@ template <> struct Tr<3> {
   static constexpr int BN = RTC_FAST_BN, TPI = 512 / RTC_FAST_BN, NBUF = RTC_FAST_NBUF, NMW = 2, G = RTC_FAST_G, XW = 8;
   static constexpr bool EARLY = false;
   static constexpr int warp_of(int l) { return l <= 1 ? 0 : 1; }
+  static constexpr size_t SMEM_CAP = 227 * 1024 - 4096;
 };
 template <int S> constexpr int nthreads() { return 32 * (NE + 2 + Tr<S>::NMW); }
 
@@ -381,8 +387,7 @@ __device__ __forceinline__ void issue_tile(uint32_t dbase, uint32_t at, uint64_t
 template <int S, bool TS, int KB>
 __device__ __forceinline__ void issue_tile_mw(int mw, uint32_t dbase, uint32_t at, uint64_t adesc, uint64_t bdesc) {
   if (mw == 0) issue_tile<S, 0, TS, KB>(dbase, at, adesc, bdesc);
-  else if (Tr<S>::NMW < 3 || mw == 1) issue_tile<S, 1, TS, KB>(dbase, at, adesc, bdesc);
-  else issue_tile<S, 2, TS, KB>(dbase, at, adesc, bdesc);
+  else issue_tile<S, 1, TS, KB>(dbase, at, adesc, bdesc);
 }
 
 // Persistent, warp-specialized.  Work item = (problem, row block, chunk of TPI tiles).
@@ -894,11 +899,12 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
     return (size_t)t.nas * S * KB * A_TILE + (size_t)nbs * S * KB * BN * BK + (size_t)nws * BM * BN * elt;
   };
   // W stages first (the HBM stream the kernel is bound by), then B stages (L2-resident slices):
-  // the first (nws, nbs) in (4, 2) x (8, 4, 2) that fits.  r = 64 FAST gets 4 W stages instead
+  // the first (nws, nbs) in (4, 2) x (8, 4, 2) within the mode's budget.  r = 64 FAST gets 4 W stages instead
   // of 2.  More than 4 W stages does not pay: PRECISE r = 32 at 8 W stages (200 KB of shared
   // memory) is no faster alone and, in lra_batch, keeps the next group's nucleus and factor CTAs
   // off the SMs (config-2 bench 9395 -> 8393 matrices/s).
   const size_t lim = 227 * 1024 - 4096;
+  const size_t cap = S == 6 ? Tr<6>::SMEM_CAP : Tr<3>::SMEM_CAP;
   t.nws = 2;
   t.nbs = 2;
   {
@@ -906,7 +912,7 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
     static const int nws_max = getenv("LRA_RTC_NWS") ? atoi(getenv("LRA_RTC_NWS")) : 4;   // diagnostics
     for (int w = nws_max; w >= 2 && !found; w >>= 1)
       for (int b = NBS; b >= 2 && !found; b >>= 1)
-        if (smem_of(w, b) <= lim) {
+        if (smem_of(w, b) <= cap) {
           t.nws = w;
           t.nbs = b;
           found = true;
@@ -914,7 +920,9 @@ cudaError_t launch_residual_tc(ResArgs a, int64_t nb, int S, void *scratch, doub
   }
   const size_t smem = smem_of(t.nws, t.nbs);
   if (smem > lim) return cudaErrorInvalidConfiguration;   // caller falls back to the fp64 SIMT pass
-  const int64_t grid = t.items < num_sms_rtc() ? t.items : num_sms_rtc();
+  static const int grid_cap = getenv("LRA_RTC_GRID") ? atoi(getenv("LRA_RTC_GRID")) : 0;   // diagnostics
+  int64_t ncta = grid_cap > 0 && grid_cap < num_sms_rtc() ? grid_cap : num_sms_rtc();
+  const int64_t grid = t.items < ncta ? t.items : ncta;
   void (*kern)(TcArgs, CUtensorMap);
   if (ts_mode)
     kern = a.dtype == LRA_F32 ? (S == 6 ? k_resid<float, 6, true> : k_resid<float, 3, true>)
