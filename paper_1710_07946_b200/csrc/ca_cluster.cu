@@ -29,6 +29,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef CC_PAIR_PRODUCT
+#define CC_PAIR_PRODUCT 1   // k_cacl2: row-pair blocked C = B G^{-1}
+#endif
+
 namespace lra {
 
 // phase counters (clock64 cycles of CTA 0 / thread 0, summed over problems):
@@ -1008,6 +1012,42 @@ __global__ void __launch_bounds__(NT, 1) k_cacl2(CAArgs a) {
         __syncwarp();
       };
       auto product = [&](double (&acc)[W]) {
+#if CC_PAIR_PRODUCT
+        if constexpr (W >= 4 && W % 4 == 0) {
+          // Row pairs (ri, ri ^ 1): each thread computes BOTH rows of the pair over half of its
+          // W columns, so every X value read from shared memory feeds two FMAs (the product was
+          // shared-memory bound: one 8-byte X read per DFMA), then swaps the other row's half
+          // with the pair partner (lane ^ TPR).  Every output is the same FMA chain over t
+          // ascending as before (bit-identical).
+          constexpr int H = W / 2;
+          const int h = (k.lane / TPR) & 1;
+          const int rp = ri ^ 1;
+          double a0[H], a1[H];
+#pragma unroll
+          for (int w = 0; w < H; ++w) a0[w] = a1[w] = 0.0;
+          for (int t = 0; t < q; ++t) {
+            const int st = t / W, wt = t - st * W;
+            const double b0 = SB[wt * NT + ri * TPR + st];
+            const double b1 = SB[wt * NT + rp * TPR + st];
+            const double2 *xr = reinterpret_cast<const double2 *>(X + t * Q + jb + h * H);
+#pragma unroll
+            for (int w = 0; w < H / 2; ++w) {
+              const double2 xv = xr[w];
+              a0[2 * w] = fma(b0, xv.x, a0[2 * w]);
+              a0[2 * w + 1] = fma(b0, xv.y, a0[2 * w + 1]);
+              a1[2 * w] = fma(b1, xv.x, a1[2 * w]);
+              a1[2 * w + 1] = fma(b1, xv.y, a1[2 * w + 1]);
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < H; ++w) {
+            const double o = __shfl_xor_sync(0xffffffffu, a1[w], TPR);   // row ri, the other half
+            acc[w] = h == 0 ? a0[w] : o;
+            acc[H + w] = h == 0 ? o : a0[w];
+          }
+          return;
+        }
+#endif
 #pragma unroll
         for (int w = 0; w < W; ++w) acc[w] = 0.0;
         for (int t = 0; t < q; ++t) {
