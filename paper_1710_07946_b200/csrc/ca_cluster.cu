@@ -1409,6 +1409,7 @@ int ca_cluster_max_active(int64_t maxN, int q) {
   }
   if (q <= 8) return cc_active_t<8, 1>(maxN);
   if (q <= 16) return cc_active_t<16, 1>(maxN);
+  if (q == 20) return cc_active_t<20, 1>(maxN);    // config 3 (k = l = 20): q as a compile-time constant
   if (q <= 24) return cc_active_t<24, 1>(maxN);
   if (q <= 32) return cc_active_t<32, 2>(maxN);
   if (q <= 48) return cc_active_t<48, 2>(maxN);
@@ -1428,6 +1429,7 @@ cudaError_t launch_ca_cluster(CAArgs a, int64_t nb, int64_t maxN, cudaStream_t s
   }
   if (a.q <= 8) return launch_cc_t<8, 1>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 16) return launch_cc_t<16, 1>(a, nb, maxN, st, cs_out, pf);
+  if (a.q == 20) return launch_cc_t<20, 1>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 24) return launch_cc_t<24, 1>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 32) return launch_cc_t<32, 2>(a, nb, maxN, st, cs_out, pf);
   if (a.q <= 48) return launch_cc_t<48, 2>(a, nb, maxN, st, cs_out, pf);

@@ -101,12 +101,15 @@ template <> struct Tr<6> {
 #ifndef RTC_FAST_BN
 #define RTC_FAST_BN 64    // FAST tile width (diagnostic builds: 32 with 4 accumulator buffers)
 #endif
+#ifndef RTC_FAST_EARLY
+#define RTC_FAST_EARLY 0
+#endif
 #ifndef RTC_FAST_NBUF
 #define RTC_FAST_NBUF 2
 #endif
 template <> struct Tr<3> {
   static constexpr int BN = RTC_FAST_BN, TPI = 512 / RTC_FAST_BN, NBUF = RTC_FAST_NBUF, NMW = 2, G = RTC_FAST_G, XW = 8;
-  static constexpr bool EARLY = false;
+  static constexpr bool EARLY = RTC_FAST_EARLY;
   static constexpr int warp_of(int l) { return l <= 1 ? 0 : 1; }
   static constexpr size_t SMEM_CAP = 227 * 1024 - 4096;
 };
