@@ -568,6 +568,40 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
     {
       CC_T0();
       const double *X = Xp + ib * Q * Q;
+#if CC_PAIR_PRODUCT
+      if constexpr (W >= 4 && W % 4 == 0) {
+        // row pairs (ri, ri ^ 1), as in k_cacl2: each X value from shared memory feeds two FMAs,
+        // the halves are swapped with the pair partner (lane ^ TPR); same FMA chains
+        constexpr int H = W / 2;
+        const int h = (k.lane / TPR) & 1;
+        const int rp = ri ^ 1;
+        const bool hp = rp < nloc;
+        const double *Prow = Cs + (size_t)(hp ? rp : 0) * QP;
+        double a0[H], a1[H];
+#pragma unroll
+        for (int w = 0; w < H; ++w) a0[w] = a1[w] = 0.0;
+        for (int t = 0; t < q; ++t) {
+          const double b0 = has ? Crow[t] : 0.0, b1 = hp ? Prow[t] : 0.0;
+          const double2 *xr = reinterpret_cast<const double2 *>(X + t * Q + jb + h * H);
+#pragma unroll
+          for (int w = 0; w < H / 2; ++w) {
+            const double2 xv = xr[w];
+            a0[2 * w] = fma(b0, xv.x, a0[2 * w]);
+            a0[2 * w + 1] = fma(b0, xv.y, a0[2 * w + 1]);
+            a1[2 * w] = fma(b1, xv.x, a1[2 * w]);
+            a1[2 * w + 1] = fma(b1, xv.y, a1[2 * w + 1]);
+          }
+        }
+        const bool live = has && myslot < 0;
+#pragma unroll
+        for (int w = 0; w < H; ++w) {
+          const double o = __shfl_xor_sync(0xffffffffu, a1[w], TPR);
+          row[w] = live ? (h == 0 ? a0[w] : o) : 0.0;
+          row[H + w] = live ? (h == 0 ? o : a0[w]) : 0.0;
+        }
+      } else
+#endif
+      {
 #pragma unroll
       for (int w = 0; w < W; ++w) row[w] = 0.0;
       if (has && myslot < 0) {
@@ -585,6 +619,7 @@ __global__ void __launch_bounds__(NT, 1) k_cacl(CAArgs a) {
             row[0] = fma(bt, X[t * Q + jb], row[0]);
           }
         }
+      }
       }
       CC_T1(4);
     }
