@@ -510,8 +510,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=90)
-    ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
-                    help="batches in flight (2: consecutive steps alternate between two handles and streams)")
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2, 3, 4],
+                    help="batches in flight (S > 1: consecutive steps rotate over S handles and streams)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "cfg3"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary workloads (cfg5, cfg3)")
@@ -577,7 +577,7 @@ def main():
     # side streams and scratch) on two streams, so one batch's tail (the last group's nucleus,
     # factors and residual) overlaps the next batch's C-A waves.  The timed region spans both
     # streams (they wait on the start event; the end event waits on both).
-    hs = [h, Handle(lrank)] if args.streams == 2 else [h]
+    hs = [h] + [Handle(lrank) for _ in range(args.streams - 1)]
     sts = [torch.cuda.Stream() for _ in hs] if len(hs) > 1 else [st]
     bufsx = [bufs] + [pipeline.BatchBuffers(B, R, K) for _ in hs[1:]]
 
