@@ -700,10 +700,23 @@ def main():
         ems = _max_over_ranks(f0.elapsed_time(f1), ws)
         d2h = sum(x.numel() * x.element_size() for x in (bufs.I, bufs.J, bufs.U, bufs.num2, bufs.den2))
         h2d = int(pools[0].numel() * 4)
+        # the host link's own rate: the same pinned batch copied alone, back to back (best of 3)
+        link = 0.0
+        for _ in range(3):
+            l0 = torch.cuda.Event(enable_timing=True)
+            l1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(cs):
+                l0.record(cs)
+                dev[0].copy_(pin[0], non_blocking=True)
+                l1.record(cs)
+            torch.cuda.synchronize()
+            link = max(link, h2d / (l0.elapsed_time(l1) / 1e3) / 1e9)
+        h2d_gbs = h2d * ke / (ems / 1e3) / 1e9
         e2e = {"value": ws * B * ke / (ems / 1e3), "unit": "matrices/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": int(d2h), "h2d_GBs_per_gpu": h2d * ke / (ems / 1e3) / 1e9,
-               "note": "H2D of batch i+1 overlaps batch i's compute; PCIe-bound when h2d_GBs_per_gpu is near "
-                       "the host link rate"}
+               "d2h_bytes_per_step": int(d2h), "h2d_GBs_per_gpu": h2d_gbs,
+               "h2d_link_GBs": link, "pcie_frac": h2d_gbs / link if link > 0 else None,
+               "note": "H2D of batch i+1 overlaps batch i's compute; pcie_frac = the step's H2D rate over the "
+                       "link rate measured alone (a pinned copy of the same batch): near 1 = PCIe-bound"}
         del dev, Wd, pin
 
     cpu = None
