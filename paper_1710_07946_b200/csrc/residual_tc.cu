@@ -158,8 +158,14 @@ __global__ void __launch_bounds__(128) k_split_ab(const double *A, const double 
   constexpr int RT = KBT * BK;                 // values per thread (zero beyond r)
   const int64_t b = blockIdx.y;
   const bool live = !(status && status[b] != LRA_OK);
-  double v[RT];
+  // r > 32: two passes over the thread's values — the maximum first, then the digits K block by
+  // K block (re-read from L1/L2) — so only 32 values are held at a time and r = 64 / 128 keep the
+  // occupancy of r = 32 (32768^2 r = 64: 53 -> 41 us).  r <= 32 keeps its values from the one pass.
+  const double *src;
+  int64_t step;                                // stride between consecutive values t
+  bool ok;
   double mx = 0.0;
+  double keep[KBT == 1 ? BK : 1];              // r <= 32: the one pass keeps its values
   signed char *base;
   int boff;
   int tile_bytes;
@@ -167,16 +173,18 @@ __global__ void __launch_bounds__(128) k_split_ab(const double *A, const double 
     const int64_t rb = blockIdx.x;
     const int i = threadIdx.x;
     const int64_t gi = rb * BM + i;
-    const bool ok = live && gi < m;
-    const double *Ab = A + b * a_stride + gi;
-#pragma unroll
-    for (int t = 0; t < RT; ++t) v[t] = (ok && t < r) ? __ldg(Ab + (int64_t)t * m) : 0.0;
-#pragma unroll
-    for (int t = 0; t < RT; ++t) mx = fmax(mx, fabs(v[t]));
+    ok = live && gi < m;
+    src = A + b * a_stride + gi;
+    step = m;
+#pragma unroll 8
+    for (int t = 0; t < RT; ++t) {
+      const double x = (ok && t < r) ? __ldg(src + (int64_t)t * step) : 0.0;
+      if constexpr (KBT == 1) keep[t] = x;
+      mx = fmax(mx, fabs(x));
+    }
     const int e = scale_exp(mx);
     if (gi < m) sa[b * m + gi] = ok ? e : -4000;     // -4000: row contributes nothing
-#pragma unroll
-    for (int t = 0; t < RT; ++t) v[t] = ldexp(v[t], -e);
+    mx = (double)e;                                  // the exponent travels in mx below
     base = Aq + (size_t)(b * RB + rb) * KBT * S * A_TILE;
     boff = (i >> 3) * 256 + (i & 7) * 16;
     tile_bytes = A_TILE;
@@ -185,12 +193,15 @@ __global__ void __launch_bounds__(128) k_split_ab(const double *A, const double 
     const int64_t cb = ((int64_t)blockIdx.x - RB) * TPC + threadIdx.x / BN;
     const int jj = threadIdx.x % BN;
     const int64_t gj = cb * BN + jj;
-    const bool ok = live && cb < CB && gj < n;
-    const double *Bb = B + b * b_stride + gj * r;
-#pragma unroll
-    for (int t = 0; t < RT; ++t) v[t] = (ok && t < r) ? __ldg(Bb + t) : 0.0;
-#pragma unroll
-    for (int t = 0; t < RT; ++t) mx = fmax(mx, fabs(v[t]));
+    ok = live && cb < CB && gj < n;
+    src = B + b * b_stride + gj * r;
+    step = 1;
+#pragma unroll 8
+    for (int t = 0; t < RT; ++t) {
+      const double x = (ok && t < r) ? __ldg(src + t) : 0.0;
+      if constexpr (KBT == 1) keep[t] = x;
+      mx = fmax(mx, fabs(x));
+    }
     // tile max: within the warp for BN <= 32, through shared memory for BN = 64 (two warps)
 #pragma unroll
     for (int o = (BN < 32 ? BN : 32) / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -204,22 +215,29 @@ __global__ void __launch_bounds__(128) k_split_ab(const double *A, const double 
     const int e = scale_exp(mx);
     if (cb >= CB) return;
     if (jj == 0) sbq[b * CB + cb] = ok ? e : -4000;
-#pragma unroll
-    for (int t = 0; t < RT; ++t) v[t] = ldexp(v[t], -e);
+    mx = (double)e;
     base = Bq + (size_t)(b * CB + cb) * KBT * S * (BN * BK);
     boff = (jj >> 3) * 256 + (jj & 7) * 16;
     tile_bytes = BN * BK;
   }
+  const int e = (int)mx;
   // digits of all values, packed 16 bytes per (kb, K half, slice)
-#pragma unroll
+#pragma unroll 1
   for (int kb = 0; kb < KBT; ++kb) {
+    double v[BK];
+#pragma unroll
+    for (int t = 0; t < BK; ++t) {
+      const int tt = kb * BK + t;
+      if constexpr (KBT == 1) v[t] = ldexp(keep[t], -e);
+      else v[t] = ldexp((ok && tt < r) ? __ldg(src + (int64_t)tt * step) : 0.0, -e);
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       uint32_t w[S][4];
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         int d[S];
-        digits256<S>(v[kb * BK + h * 16 + kk], d);
+        digits256<S>(v[h * 16 + kk], d);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           const uint32_t byte = ((uint32_t)d[s] & 0xffu) << (8 * (kk & 3));
